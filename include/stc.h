@@ -1,0 +1,148 @@
+/* stc.h — C ABI of the B200-native sparse-contraction library (libstc.so).
+ *
+ * The reference (arxiv 2405.16883 "Scorch", package `sparsetc`) has no native
+ * layer: its hot path is the Python interpreter in
+ * /root/reference/pkg/src/sparsetc/engine.py. Each entry point below replaces
+ * one interpreted loop nest of that engine; the citation names it.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers (CUDA global memory) except `stream`,
+ *     which is a cudaStream_t passed as void*. The library never allocates or
+ *     frees: scratch comes from a caller-provided workspace whose size is
+ *     given by the matching *_workspace_bytes query.
+ *   - Indices are int32, values float32, leading dimensions in elements.
+ *   - Launches are asynchronous and stream-ordered; nothing synchronises.
+ *   - Return 0 on success, negative on error (STC_E*); the message is
+ *     available from stc_last_error() (thread-local). No exceptions cross
+ *     the ABI. There is no CPU fallback.
+ *   - Results are deterministic: no atomics; every output row is reduced in
+ *     a fixed order.
+ */
+#ifndef STC_H_
+#define STC_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STC_ABI_VERSION 1
+
+#define STC_OK 0
+#define STC_EINVAL (-1)       /* null / misaligned pointer, bad shape        */
+#define STC_EUNSUPPORTED (-2) /* shape or variant not supported             */
+#define STC_ELAUNCH (-3)      /* CUDA launch error (cudaGetLastError)       */
+#define STC_EWORKSPACE (-4)   /* workspace too small                        */
+
+/* SpMM kernel variants — the device form of the reference planner's choice
+ * of loop order and tiling (scheduler.py:347, tiling.py:53):
+ *   ROW     one sub-warp per row (loop order [i,j,k], rows uniform)
+ *   MERGE   nnz-balanced merge-path split with atomics-free carries
+ *           (same loop order, power-law rows)
+ *   COLTILE column-tiled, dense operand staged in shared memory
+ *           (tile set {k} with a wide k)                                    */
+#define STC_VARIANT_ROW 0
+#define STC_VARIANT_MERGE 1
+#define STC_VARIANT_COLTILE 2
+
+#define STC_EPILOGUE_NONE 0
+#define STC_EPILOGUE_RELU 1
+
+int stc_abi_version(void);
+const char* stc_last_error(void);
+
+/* Number of kernels this library has launched in the process (all threads).
+ * Used by bench.py to report how many native launches a timed region made. */
+long long stc_launch_count(void);
+
+/* Merge-path partition of a compressed row structure (plan time).
+ * Groups own `items_per_group` consecutive items of the merged sequence
+ * (m row ends + nnz entries). Writes (row, pos) int pairs for groups
+ * 0..n_groups into `starts` (2*(n_groups+1) ints).                           */
+long long stc_merge_path_groups(int m, long long nnz, int items_per_group);
+int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
+                             int* starts, void* stream);
+
+/* Workspace for the MERGE variant (carry buffers); 0 for ROW/COLTILE.        */
+size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int items_per_group,
+                                int batch);
+
+/* CSR SpMM  C[i,:] = act(sum_{p in row i} vals[p] * B[colidx[p], :] + D[i,:])
+ * Replaces the dense-output driver + vectorised tail of the reference,
+ * engine.py:487-573 (`_run_dense_output`, `vector_sink`), for
+ * C(i,k) = A(i,j) * B(j,k) [+ D(i,k)] with A CSR, B/D dense.
+ * n = columns of A (rows of B); D nullable; partition required for MERGE.   */
+int stc_spmm_csr_f32(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
+                     long long nnz, const float* B, long long ldb, float* C, long long ldc,
+                     const float* D, long long ldd, int variant, int epilogue, const int* partition,
+                     int items_per_group, void* ws, size_t ws_bytes, void* stream);
+
+/* Batched CSR SpMM over a shared structure (multi-head O(h,i,d)=P(h,i,j)*V(h,j,d),
+ * reference plan [dense,dense,compressed] x dense, engine.py:487-573):
+ * per batch z the values start at vals + z*val_bstride, B at B + z*b_bstride,
+ * C (and D) at C + z*c_bstride.                                              */
+int stc_spmm_csr_batched_f32(int batch, int m, int n, int k, const int* rowptr, const int* colidx,
+                             const float* vals, long long nnz, long long val_bstride,
+                             const float* B, long long ldb, long long b_bstride, float* C,
+                             long long ldc, long long c_bstride, int variant, int epilogue,
+                             const int* partition, int items_per_group, void* ws, size_t ws_bytes,
+                             void* stream);
+
+/* Distinct-row segmentation of a sorted COO row column (plan time):
+ * seg_rows[s] = s-th distinct row, seg_ptr[s] = its first entry,
+ * seg_ptr[n_seg] = nnz; *n_seg_out (device int) = number of segments.
+ * This is the compressed i-level the reference builds for a COO/DCSR SpMM
+ * or MTTKRP output (`_SparseOutputBuilder`, engine.py:233-253).             */
+size_t stc_coo_segments_temp_bytes(long long nnz);
+int stc_coo_segments(long long nnz, const int* rows, int* seg_rows, int* seg_ptr, int* n_seg_out,
+                     void* temp, size_t temp_bytes, void* stream);
+
+/* COO SpMM over precomputed segments: C[s,:] = sum_{p in seg s} vals[p]*B[cols[p],:].
+ * Output is the dense level of the reference's [compressed, dense] result
+ * (engine.py:577-644 with a 1-D Workspace, engine.py:71-90).                */
+int stc_spmm_coo_f32(int n_seg, int n, int k, const int* seg_ptr, const int* cols,
+                     const float* vals, long long nnz, const float* B, long long ldb, float* C,
+                     long long ldc, int variant, const int* partition, int items_per_group, void* ws,
+                     size_t ws_bytes, void* stream);
+
+/* SDDMM  S[h,p] = scale * maskvals[p] * dot(Q[h,i,:], K[h,colidx[p],:])
+ * (maskvals nullable = 1.0). Replaces `_run_sparse_output` + the vectorised
+ * reduction tail, engine.py:577-644 and :413-432, for
+ * S(i,j) = M(i,j) * Q(i,d) * K(j,d). d in {4,8,16,32,64,128}.               */
+int stc_sddmm_csr_f32(int m, int n, int d, int heads, const int* rowptr, const int* colidx,
+                      const float* maskvals, long long nnz, const float* Q, long long q_hs,
+                      long long q_rs, const float* K, long long k_hs, long long k_rs, float scale,
+                      float* out_vals, void* stream);
+
+/* Row-segmented softmax of each row's stored values, in place, for `heads`
+ * consecutive [nnz] value arrays. No reference symbol (the grammar has only
+ * + and *); restated in oracle/.                          */
+int stc_segsoftmax_csr_f32(int m, int heads, const int* rowptr, long long nnz, float* vals,
+                           void* stream);
+
+/* Fused sparse attention O = softmax_rows(scale * M .* (Q K^T)) V with an
+ * online softmax; S and P (nullable) are written only when non-null
+ * (parity mode). Composition of the three reference expressions SDDMM,
+ * softmax and SpMM (engine.py:577-644, 487-573).                            */
+int stc_sparse_attention_f32(int m, int n, int d, int heads, const int* rowptr, const int* colidx,
+                             const float* maskvals, long long nnz, const float* Q, long long q_hs,
+                             long long q_rs, const float* K, long long k_hs, long long k_rs,
+                             const float* V, long long v_hs, long long v_rs, float scale, float* O,
+                             long long o_hs, long long o_rs, float* S, float* P, void* stream);
+
+/* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
+ * M[s,:] = sum_{p in seg s} (vals[p] * B[j[p],:]) * C[k[p],:]
+ * Replaces `_run_sparse_output` with the (i,r) Workspace, engine.py:577-644,
+ * 71-90, for M(i,r) = T(i,j,k) * B(j,r) * C(k,r).                           */
+int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
+                        const float* vals, long long nnz, const float* B, long long ldb,
+                        const float* C, long long ldcf, float* M, long long ldm, int variant,
+                        const int* partition, int items_per_group, void* ws, size_t ws_bytes,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STC_H_ */

@@ -1,0 +1,129 @@
+"""ctypes binding of ``libstc.so`` (declared in ``include/stc.h``).
+
+Every call passes raw device pointers (``tensor.data_ptr()``) and the
+caller's current CUDA stream; the library never allocates. Negative return
+codes become Python exceptions that mirror the reference's error types
+(`ShapeError` / `ValueError` / `RuntimeError`, cf. tensor.py:20, tiling.py:55).
+There is no fallback: if the library or a GPU is missing, ``lib()`` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import torch
+
+from .tensor import ShapeError
+
+_LIB_PATH = Path(__file__).resolve().parent / "libstc.so"
+_lock = threading.Lock()
+_lib = None
+
+STC_OK = 0
+STC_EINVAL = -1
+STC_EUNSUPPORTED = -2
+STC_ELAUNCH = -3
+STC_EWORKSPACE = -4
+
+VARIANT_ROW = 0
+VARIANT_MERGE = 1
+VARIANT_COLTILE = 2
+VARIANTS = {"row": VARIANT_ROW, "merge": VARIANT_MERGE, "coltile": VARIANT_COLTILE}
+
+EPILOGUE_NONE = 0
+EPILOGUE_RELU = 1
+
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_ll = ctypes.c_longlong
+_f = ctypes.c_float
+_sz = ctypes.c_size_t
+
+# name -> (restype, argtypes); kept in the same order as include/stc.h
+SIGNATURES = {
+    "stc_abi_version": (_i, []),
+    "stc_last_error": (ctypes.c_char_p, []),
+    "stc_launch_count": (_ll, []),
+    "stc_merge_path_groups": (_ll, [_i, _ll, _i]),
+    "stc_merge_path_partition": (_i, [_i, _ll, _p, _i, _p, _p]),
+    "stc_spmm_workspace_bytes": (_sz, [_i, _ll, _i, _i, _i, _i]),
+    "stc_spmm_csr_f32": (_i, [_i, _i, _i, _p, _p, _p, _ll, _p, _ll, _p, _ll, _p, _ll, _i, _i, _p, _i,
+                              _p, _sz, _p]),
+    "stc_spmm_csr_batched_f32": (_i, [_i, _i, _i, _i, _p, _p, _p, _ll, _ll, _p, _ll, _ll, _p, _ll, _ll,
+                                      _i, _i, _p, _i, _p, _sz, _p]),
+    "stc_coo_segments_temp_bytes": (_sz, [_ll]),
+    "stc_coo_segments": (_i, [_ll, _p, _p, _p, _p, _p, _sz, _p]),
+    "stc_spmm_coo_f32": (_i, [_i, _i, _i, _p, _p, _p, _ll, _p, _ll, _p, _ll, _i, _p, _i, _p, _sz, _p]),
+    "stc_sddmm_csr_f32": (_i, [_i, _i, _i, _i, _p, _p, _p, _ll, _p, _ll, _ll, _p, _ll, _ll, _f, _p, _p]),
+    "stc_segsoftmax_csr_f32": (_i, [_i, _i, _p, _ll, _p, _p]),
+    "stc_sparse_attention_f32": (_i, [_i, _i, _i, _i, _p, _p, _p, _ll, _p, _ll, _ll, _p, _ll, _ll, _p,
+                                      _ll, _ll, _f, _p, _ll, _ll, _p, _p, _p]),
+    "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _p, _ll, _p, _ll, _p, _ll, _i, _p, _i, _p,
+                                 _sz, _p]),
+}
+
+
+class ExtensionUnavailable(RuntimeError):
+    """libstc.so is missing or no CUDA device is present; nothing falls back."""
+
+
+def load_library(path: Path | None = None) -> ctypes.CDLL:
+    """Open the shared object and attach the C signatures (no GPU needed)."""
+    path = Path(path) if path is not None else _LIB_PATH
+    if not path.exists():
+        raise ExtensionUnavailable(
+            f"{path} not found: build it with `python -m paper_2405_16883_b200._build` "
+            "(the CUDA path has no CPU fallback)"
+        )
+    lib = ctypes.CDLL(str(path))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                _lib = load_library()
+    return _lib
+
+
+def require_cuda(*tensors: torch.Tensor) -> None:
+    if not torch.cuda.is_available():
+        raise ExtensionUnavailable("no CUDA device: sparse contractions run only on the GPU")
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise ExtensionUnavailable(
+                "operand buffers are on the CPU; move the tensor to CUDA (tensor.to('cuda'))"
+            )
+
+
+def check(rc: int, what: str) -> None:
+    if rc == STC_OK:
+        return
+    msg = lib().stc_last_error().decode(errors="replace")
+    text = f"{what}: {msg} (code {rc})"
+    if rc == STC_EINVAL:
+        raise ShapeError(text)
+    if rc == STC_EUNSUPPORTED:
+        raise ValueError(text)
+    raise RuntimeError(text)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def launch_count() -> int:
+    """Kernels launched so far by libstc.so in this process."""
+    return int(lib().stc_launch_count())

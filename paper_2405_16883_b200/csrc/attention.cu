@@ -1,0 +1,113 @@
+// C-ABI entry points for SDDMM, segmented softmax and fused sparse attention.
+#include "abi_util.cuh"
+#include "attention.cuh"
+
+using namespace stc;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int check_common(int m, int n, int d, int heads, const int* rowptr, long long nnz) {
+  if (m < 0 || n < 0 || d < 0 || heads < 1 || nnz < 0) return fail(STC_EINVAL, "negative extent");
+  if (nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "nnz exceeds int32 index range");
+  if (heads > 65535) return fail(STC_EUNSUPPORTED, "more than 65535 heads");
+  if (m && !rowptr) return fail(STC_EINVAL, "null rowptr");
+  return STC_OK;
+}
+
+bool dim_ok(int d) { return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128; }
+
+template <int G>
+int launch_sddmm(const AttnArgs& a, cudaStream_t st) {
+  const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
+  sddmm_kernel<G><<<grid, kThreads, 0, st>>>(a);
+  return check_launch("sddmm_kernel");
+}
+
+template <int G, bool WS>
+int launch_attn(const AttnArgs& a, cudaStream_t st) {
+  const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
+  attention_kernel<G, WS><<<grid, kThreads, 0, st>>>(a);
+  return check_launch("attention_kernel");
+}
+
+template <bool WS>
+int attn_by_d(const AttnArgs& a, cudaStream_t st) {
+  switch (a.d / 4) {
+    case 1: return launch_attn<1, WS>(a, st);
+    case 2: return launch_attn<2, WS>(a, st);
+    case 4: return launch_attn<4, WS>(a, st);
+    case 8: return launch_attn<8, WS>(a, st);
+    case 16: return launch_attn<16, WS>(a, st);
+    default: return launch_attn<32, WS>(a, st);
+  }
+}
+
+}  // namespace
+
+extern "C" int stc_sddmm_csr_f32(int m, int n, int d, int heads, const int* rowptr, const int* colidx,
+                                 const float* maskvals, long long nnz, const float* Q, long long q_hs,
+                                 long long q_rs, const float* K, long long k_hs, long long k_rs, float scale,
+                                 float* out_vals, void* stream) {
+  int rc = check_common(m, n, d, heads, rowptr, nnz);
+  if (rc) return rc;
+  if (m == 0 || nnz == 0) return STC_OK;
+  if (!dim_ok(d)) return fail(STC_EUNSUPPORTED, "head dim %d not in {4,8,16,32,64,128}", d);
+  if (!colidx || !Q || !K || !out_vals) return fail(STC_EINVAL, "null pointer");
+  if (!aligned16(Q) || !aligned16(K) || q_rs % 4 || k_rs % 4 || q_hs % 4 || k_hs % 4 || q_rs < d || k_rs < d)
+    return fail(STC_EINVAL, "Q/K must be 16-byte aligned with strides that are multiples of 4 and >= d");
+  AttnArgs a{};
+  a.m = m; a.n = n; a.d = d; a.heads = heads;
+  a.rowptr = rowptr; a.colidx = colidx; a.maskv = maskvals;
+  a.Q = Q; a.q_hs = q_hs; a.q_rs = q_rs;
+  a.K = K; a.k_hs = k_hs; a.k_rs = k_rs;
+  a.scale = scale; a.nnz = nnz; a.S = out_vals;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (d / 4) {
+    case 1: return launch_sddmm<1>(a, st);
+    case 2: return launch_sddmm<2>(a, st);
+    case 4: return launch_sddmm<4>(a, st);
+    case 8: return launch_sddmm<8>(a, st);
+    case 16: return launch_sddmm<16>(a, st);
+    default: return launch_sddmm<32>(a, st);
+  }
+}
+
+extern "C" int stc_segsoftmax_csr_f32(int m, int heads, const int* rowptr, long long nnz, float* vals,
+                                      void* stream) {
+  int rc = check_common(m, 0, 0, heads, rowptr, nnz);
+  if (rc) return rc;
+  if (m == 0 || nnz == 0) return STC_OK;
+  if (!vals) return fail(STC_EINVAL, "null pointer");
+  const dim3 grid((unsigned)ceil_div((long long)m * 32, kThreads), heads);
+  segsoftmax_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(m, nnz, rowptr, vals);
+  return check_launch("segsoftmax_kernel");
+}
+
+extern "C" int stc_sparse_attention_f32(int m, int n, int d, int heads, const int* rowptr, const int* colidx,
+                                        const float* maskvals, long long nnz, const float* Q, long long q_hs,
+                                        long long q_rs, const float* K, long long k_hs, long long k_rs,
+                                        const float* V, long long v_hs, long long v_rs, float scale, float* O,
+                                        long long o_hs, long long o_rs, float* S, float* P, void* stream) {
+  int rc = check_common(m, n, d, heads, rowptr, nnz);
+  if (rc) return rc;
+  if (m == 0) return STC_OK;
+  if (!dim_ok(d)) return fail(STC_EUNSUPPORTED, "head dim %d not in {4,8,16,32,64,128}", d);
+  if (!O || (nnz && (!colidx || !Q || !K || !V))) return fail(STC_EINVAL, "null pointer");
+  if (P && !S) return fail(STC_EINVAL, "P output requires the S buffer");
+  const bool ok = aligned16(Q) && aligned16(K) && aligned16(V) && aligned16(O) && q_rs % 4 == 0 &&
+                  k_rs % 4 == 0 && v_rs % 4 == 0 && o_rs % 4 == 0 && q_hs % 4 == 0 && k_hs % 4 == 0 &&
+                  v_hs % 4 == 0 && o_hs % 4 == 0 && q_rs >= d && k_rs >= d && v_rs >= d && o_rs >= d;
+  if (!ok) return fail(STC_EINVAL, "Q/K/V/O must be 16-byte aligned with strides multiple of 4 and >= d");
+  AttnArgs a{};
+  a.m = m; a.n = n; a.d = d; a.heads = heads;
+  a.rowptr = rowptr; a.colidx = colidx; a.maskv = maskvals;
+  a.Q = Q; a.q_hs = q_hs; a.q_rs = q_rs;
+  a.K = K; a.k_hs = k_hs; a.k_rs = k_rs;
+  a.V = V; a.v_hs = v_hs; a.v_rs = v_rs;
+  a.scale = scale; a.nnz = nnz; a.S = S; a.P = P;
+  a.O = O; a.o_hs = o_hs; a.o_rs = o_rs;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return S ? attn_by_d<true>(a, st) : attn_by_d<false>(a, st);
+}

@@ -1,0 +1,184 @@
+// K5 SDDMM, K6 row-segmented softmax and K7 fused sparse attention (sm_100a).
+//
+// Layout: one shared CSR mask (rowptr/colidx[/maskvals]) for all heads;
+// Q [H][M][d], K/V [H][N][d] row-major (head strides given), scores/probs as
+// [H][nnz] value arrays in the mask's order, O [H][M][d].
+//
+// A group of G = d/4 lanes owns one (head, row); each lane holds a float4 slice
+// of q. For a batch of G stored entries every lane forms G partial dot
+// products from G independent K-row gathers (G LDG.128 in flight per lane),
+// then a transposed butterfly (G-1 shuffles) leaves the full dot product of
+// entry l in lane l. The fused kernel keeps an online (running max / running
+// sum) softmax and accumulates p * V_j without materialising S or P.
+#pragma once
+
+#include "stc_common.cuh"
+
+namespace stc {
+
+struct AttnArgs {
+  int m, n, d, heads;
+  const int* rowptr;
+  const int* colidx;
+  const float* maskv;      // nullable: implicit 1.0
+  const float* Q;
+  long long q_hs, q_rs;    // head / row strides (elements)
+  const float* K;
+  long long k_hs, k_rs;
+  const float* V;
+  long long v_hs, v_rs;
+  float scale;
+  long long nnz;
+  float* S;                // [H][nnz] nullable (fused: written only if non-null)
+  float* P;                // [H][nnz] nullable
+  float* O;                // [H][M][d]
+  long long o_hs, o_rs;
+};
+
+// v[i] over lanes -> lane l holds sum over the group of the partials for entry l.
+template <int G>
+STC_DEVICE float transpose_reduce(float (&v)[G], int lane, unsigned mask) {
+#pragma unroll
+  for (int h = G / 2; h >= 1; h >>= 1) {
+    const bool upper = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = upper ? v[i] : v[i + h];
+      const float keep = upper ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(mask, send, h, G);
+    }
+  }
+  return v[0];
+}
+
+template <int G>
+STC_DEVICE float group_max(float x, unsigned mask) {
+#pragma unroll
+  for (int h = G / 2; h >= 1; h >>= 1) x = fmaxf(x, __shfl_xor_sync(mask, x, h, G));
+  return x;
+}
+template <int G>
+STC_DEVICE float group_sum(float x, unsigned mask) {
+#pragma unroll
+  for (int h = G / 2; h >= 1; h >>= 1) x += __shfl_xor_sync(mask, x, h, G);
+  return x;
+}
+
+// SDDMM: S[h, p] = scale * mask[p] * dot(Q[h,i,:], K[h,col[p],:])
+template <int G>
+__global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
+  const int lane = threadIdx.x % G;
+  const unsigned mask = subwarp_mask<G>();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int h = blockIdx.y;
+  if (row >= a.m) return;
+  const uint64_t pol = policy_evict_last();
+  const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
+  const float* Kh = a.K + h * a.k_hs + lane * 4;
+  float* out = a.S + h * a.nnz;
+  const int start = a.rowptr[row], end = a.rowptr[row + 1];
+  for (int base = start; base < end; base += G) {
+    const int n = min(G, end - base);
+    const int my_col = (lane < n) ? ld_stream(a.colidx + base + lane) : 0;
+    float part[G];
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int c = __shfl_sync(mask, my_col, t, G);
+      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < n) kv = ld_gather4(Kh + (long long)c * a.k_rs, pol);
+      part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
+    }
+    const float s = transpose_reduce<G>(part, lane, mask);
+    if (lane < n) {
+      const float mv = a.maskv ? ld_stream(a.maskv + base + lane) : 1.f;
+      st_stream1(out + base + lane, s * mv * a.scale);
+    }
+  }
+}
+
+// Row-segmented softmax over each row's stored entries, in place, all heads.
+__global__ void __launch_bounds__(256) segsoftmax_kernel(int m, long long nnz, const int* __restrict__ rowptr,
+                                                         float* __restrict__ vals) {
+  const int lane = threadIdx.x % 32;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int h = blockIdx.y;
+  if (row >= m) return;
+  float* v = vals + h * nnz;
+  const int start = rowptr[row], end = rowptr[row + 1];
+  float mx = -INFINITY;
+  for (int p = start + lane; p < end; p += 32) mx = fmaxf(mx, v[p]);
+  mx = group_max<32>(mx, 0xffffffffu);
+  float sum = 0.f;
+  for (int p = start + lane; p < end; p += 32) sum += expf(v[p] - mx);
+  sum = group_sum<32>(sum, 0xffffffffu);
+  const float inv = 1.f / sum;
+  for (int p = start + lane; p < end; p += 32) v[p] = expf(v[p] - mx) * inv;
+}
+
+// Fused: O[h,i,:] = sum_j softmax_j(scale * m_ij * q_i.k_j) * v_j with an online softmax.
+template <int G, bool WRITE_S>
+__global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
+  const int lane = threadIdx.x % G;
+  const unsigned mask = subwarp_mask<G>();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int h = blockIdx.y;
+  if (row >= a.m) return;
+  const uint64_t pol = policy_evict_last();
+  const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
+  const float* Kh = a.K + h * a.k_hs + lane * 4;
+  const float* Vh = a.V + h * a.v_hs + lane * 4;
+  const int start = a.rowptr[row], end = a.rowptr[row + 1];
+  float run_max = -INFINITY, run_sum = 0.f;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = start; base < end; base += G) {
+    const int n = min(G, end - base);
+    const int my_col = (lane < n) ? ld_stream(a.colidx + base + lane) : 0;
+    float part[G];
+    float4 vv[G];
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int c = __shfl_sync(mask, my_col, t, G);
+      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
+      vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < n) {
+        kv = ld_gather4(Kh + (long long)c * a.k_rs, pol);
+        vv[t] = ld_gather4(Vh + (long long)c * a.v_rs, pol);
+      }
+      part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
+    }
+    float s = transpose_reduce<G>(part, lane, mask);
+    const float mv = (lane < n && a.maskv) ? ld_stream(a.maskv + base + lane) : 1.f;
+    s = (lane < n) ? s * mv * a.scale : -INFINITY;
+    if constexpr (WRITE_S) {
+      if (lane < n) a.S[h * a.nnz + base + lane] = s;
+    }
+    const float bmax = group_max<G>(s, mask);
+    const float new_max = fmaxf(run_max, bmax);
+    const float p = (lane < n) ? expf(s - new_max) : 0.f;
+    const float corr = expf(run_max - new_max);  // 0 on the first batch (run_max = -inf)
+    run_sum = run_sum * corr + group_sum<G>(p, mask);
+    o.x *= corr; o.y *= corr; o.z *= corr; o.w *= corr;
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const float pt = __shfl_sync(mask, p, t, G);
+      o.x = fmaf(pt, vv[t].x, o.x);
+      o.y = fmaf(pt, vv[t].y, o.y);
+      o.z = fmaf(pt, vv[t].z, o.z);
+      o.w = fmaf(pt, vv[t].w, o.w);
+    }
+    run_max = new_max;
+  }
+  const float inv = run_sum > 0.f ? 1.f / run_sum : 0.f;
+  o.x *= inv; o.y *= inv; o.z *= inv; o.w *= inv;
+  st_stream4(a.O + h * a.o_hs + (long long)row * a.o_rs + lane * 4, o);
+  if constexpr (WRITE_S) {
+    // P = exp(S - max) / sum, from the scores this group just wrote (parity mode)
+    if (a.P) {
+      __syncwarp(mask);
+      for (int p = start + lane; p < end; p += G)
+        a.P[h * a.nnz + p] = expf(a.S[h * a.nnz + p] - run_max) * inv;
+    }
+  }
+}
+
+}  // namespace stc

@@ -1,0 +1,304 @@
+// C-ABI entry points for the segmented gather-reduce family:
+// CSR SpMM (ROW / MERGE / COLTILE), batched CSR SpMM, COO SpMM, MTTKRP,
+// plus the plan-time merge-path partition and COO row segmentation.
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "abi_util.cuh"
+#include "coltile.cuh"
+#include "segreduce.cuh"
+
+using namespace stc;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int choose_subw(int k, int vec) {
+  for (int s : {4, 8, 16}) {
+    if (s * vec >= k) return s;
+  }
+  return 32;
+}
+
+long long n_groups_for(int m, long long nnz, int ipg) { return ceil_div((long long)m + nnz, ipg); }
+
+size_t merge_ws_bytes(int m, long long nnz, int k, int subw, int vec, int ipg, int batch) {
+  const long long groups = n_groups_for(m, nnz, ipg);
+  const int ng = kThreads / subw;
+  const long long n_cta = ceil_div(groups, ng);
+  const int sw = subw * vec;
+  const long long slabs = ceil_div(k, sw);
+  return (size_t)(2LL * batch * slabs * n_cta * sw * (long long)sizeof(float));
+}
+
+struct Launch {
+  int variant;
+  int batch;
+  cudaStream_t stream;
+};
+
+template <int SUBW, int VEC, int EPI, bool ADD, class Op>
+int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
+  constexpr int SW = SUBW * VEC;
+  constexpr int U = SUBW >= 8 ? 8 : 4;
+  const int slabs = (int)ceil_div(o.k, SW);
+  if (o.m == 0 || slabs == 0) return STC_OK;
+  if (L.variant == STC_VARIANT_ROW) {
+    const dim3 grid((unsigned)ceil_div((long long)o.m * SUBW, kThreads), slabs, L.batch);
+    row_kernel<SUBW, VEC, EPI, ADD, U, Op><<<grid, kThreads, 0, L.stream>>>(o, ms, op);
+    return check_launch("row_kernel");
+  }
+  constexpr int NG = kThreads / SUBW;
+  ms.n_cta = (int)ceil_div(ms.n_groups, NG);
+  if (ms.n_cta == 0) return STC_OK;
+  const dim3 grid(ms.n_cta, slabs, L.batch);
+  merge_kernel<SUBW, VEC, EPI, ADD, U, Op><<<grid, kThreads, 0, L.stream>>>(o, ms, op);
+  int rc = check_launch("merge_kernel");
+  if (rc || ms.n_cta < 2) return rc;
+  const dim3 fgrid((unsigned)ceil_div((long long)(ms.n_cta - 1) * SUBW, kThreads), slabs, L.batch);
+  merge_fixup_kernel<SUBW, VEC, EPI, ADD><<<fgrid, kThreads, 0, L.stream>>>(o, ms);
+  return check_launch("merge_fixup_kernel");
+}
+
+template <int VEC, int EPI, bool ADD, template <int> class OpT>
+int dispatch_subw(int subw, const SegOut& o, const MergeShape& ms, const OpT<VEC>& op, const Launch& L) {
+  switch (subw) {
+    case 4: return launch_seg<4, VEC, EPI, ADD>(o, ms, op, L);
+    case 8: return launch_seg<8, VEC, EPI, ADD>(o, ms, op, L);
+    case 16: return launch_seg<16, VEC, EPI, ADD>(o, ms, op, L);
+    default: return launch_seg<32, VEC, EPI, ADD>(o, ms, op, L);
+  }
+}
+
+template <int VEC>
+int dispatch_spmm(int epilogue, bool add, const SegOut& o, const MergeShape& ms, const SpmmOp<VEC>& op,
+                  const Launch& L) {
+  const int subw = choose_subw(o.k, VEC);
+  if (epilogue == STC_EPILOGUE_RELU)
+    return add ? dispatch_subw<VEC, EPI_RELU, true>(subw, o, ms, op, L)
+               : dispatch_subw<VEC, EPI_RELU, false>(subw, o, ms, op, L);
+  return add ? dispatch_subw<VEC, EPI_NONE, true>(subw, o, ms, op, L)
+             : dispatch_subw<VEC, EPI_NONE, false>(subw, o, ms, op, L);
+}
+
+template <int EPI, bool ADD>
+int launch_coltile(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
+                   const float* B, long long ldb, float* C, long long ldc, const float* D, long long ldd,
+                   cudaStream_t st) {
+  const size_t smem = 2 * CT_CHUNK * CT_COLS * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(coltile_kernel<EPI, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  if (m == 0 || k == 0) return STC_OK;
+  const dim3 grid((unsigned)ceil_div(m, CT_ROWS), (unsigned)ceil_div(k, CT_COLS));
+  coltile_kernel<EPI, ADD><<<grid, 256, smem, st>>>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd);
+  return check_launch("coltile_kernel");
+}
+
+// Shared validation + dispatch for every SpMM-shaped entry point.
+int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
+                long long nnz, long long val_bs, const float* B, long long ldb, long long b_bs, float* C,
+                long long ldc, long long c_bs, const float* D, long long ldd, int variant, int epilogue,
+                const int* partition, int ipg, void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || n < 0 || k < 0 || nnz < 0 || batch < 1) return fail(STC_EINVAL, "negative extent");
+  if (nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "nnz exceeds int32 index range");
+  if (m == 0 || k == 0) return STC_OK;
+  if (!rowptr || !C || (nnz && (!colidx || !vals || !B))) return fail(STC_EINVAL, "null pointer");
+  if (ldb < k || ldc < k || (D && ldd < k)) return fail(STC_EINVAL, "leading dimension smaller than k");
+  if (epilogue != STC_EPILOGUE_NONE && epilogue != STC_EPILOGUE_RELU)
+    return fail(STC_EINVAL, "unknown epilogue %d", epilogue);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec4 = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C) &&
+                    (!D || (ldd % 4 == 0 && aligned16(D))) && (val_bs % 4 == 0 || batch == 1) &&
+                    (b_bs % 4 == 0) && (c_bs % 4 == 0);
+
+  if (variant == STC_VARIANT_COLTILE) {
+    if (!vec4) return fail(STC_EUNSUPPORTED, "COLTILE needs k, ldb, ldc multiples of 4 and 16-byte alignment");
+    if (batch != 1) return fail(STC_EUNSUPPORTED, "COLTILE is not batched");
+    if (epilogue == STC_EPILOGUE_RELU)
+      return D ? launch_coltile<EPI_RELU, true>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st)
+               : launch_coltile<EPI_RELU, false>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st);
+    return D ? launch_coltile<EPI_NONE, true>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st)
+             : launch_coltile<EPI_NONE, false>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st);
+  }
+  if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
+    return fail(STC_EINVAL, "unknown variant %d", variant);
+
+  SegOut o{m, k, rowptr, C, ldc, D, ldd};
+  MergeShape ms{};
+  ms.batch_val_stride = val_bs;
+  ms.batch_b_stride = b_bs;
+  ms.batch_c_stride = c_bs;
+  if (variant == STC_VARIANT_MERGE) {
+    if (!partition) return fail(STC_EINVAL, "MERGE variant needs a partition");
+    if (ipg < 1) return fail(STC_EINVAL, "items_per_group must be >= 1");
+    const int vec = vec4 ? 4 : 1;
+    const size_t need = merge_ws_bytes(m, nnz, k, choose_subw(k, vec), vec, ipg, batch);
+    if (ws_bytes < need || (need && !ws))
+      return fail(STC_EWORKSPACE, "workspace %zu bytes < %zu required", ws_bytes, need);
+    const int sw = choose_subw(k, vec) * vec;
+    const long long n_cta = ceil_div(n_groups_for(m, nnz, ipg), kThreads / choose_subw(k, vec));
+    const long long slabs = ceil_div(k, sw);
+    ms.starts = reinterpret_cast<const int2*>(partition);
+    ms.n_groups = (int)n_groups_for(m, nnz, ipg);
+    ms.ipg = ipg;
+    ms.head_buf = static_cast<float*>(ws);
+    ms.tail_buf = ms.head_buf + (long long)batch * slabs * n_cta * sw;
+  }
+  Launch L{variant, batch, st};
+  if (vec4) {
+    SpmmOp<4> op{colidx, vals, B, ldb};
+    return dispatch_spmm<4>(epilogue, D != nullptr, o, ms, op, L);
+  }
+  SpmmOp<1> op{colidx, vals, B, ldb};
+  return dispatch_spmm<1>(epilogue, D != nullptr, o, ms, op, L);
+}
+
+}  // namespace
+
+extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {
+  if (items_per_group < 1 || m < 0 || nnz < 0) return -1;
+  return n_groups_for(m, nnz, items_per_group);
+}
+
+extern "C" int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
+                                        int* starts, void* stream) {
+  if (m < 0 || nnz < 0 || items_per_group < 1) return fail(STC_EINVAL, "bad partition arguments");
+  if (!rowptr || !starts) return fail(STC_EINVAL, "null pointer");
+  if (((uintptr_t)starts & 7u) != 0) return fail(STC_EINVAL, "starts must be 8-byte aligned");
+  const long long groups = n_groups_for(m, nnz, items_per_group);
+  if (groups > INT32_MAX - 1) return fail(STC_EUNSUPPORTED, "too many groups");
+  const long long n = groups + 1;
+  merge_partition_kernel<<<(unsigned)ceil_div(n, kThreads), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      m, nnz, rowptr, items_per_group, (int)groups, reinterpret_cast<int2*>(starts));
+  return check_launch("merge_partition_kernel");
+}
+
+extern "C" size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int items_per_group,
+                                           int batch) {
+  if (variant != STC_VARIANT_MERGE || items_per_group < 1 || m <= 0 || k <= 0) return 0;
+  const size_t a = merge_ws_bytes(m, nnz, k, choose_subw(k, 4), 4, items_per_group, batch < 1 ? 1 : batch);
+  const size_t b = merge_ws_bytes(m, nnz, k, choose_subw(k, 1), 1, items_per_group, batch < 1 ? 1 : batch);
+  return a > b ? a : b;
+}
+
+extern "C" int stc_spmm_csr_f32(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
+                                long long nnz, const float* B, long long ldb, float* C, long long ldc,
+                                const float* D, long long ldd, int variant, int epilogue,
+                                const int* partition, int items_per_group, void* ws, size_t ws_bytes,
+                                void* stream) {
+  return spmm_common(1, m, n, k, rowptr, colidx, vals, nnz, 0, B, ldb, 0, C, ldc, 0, D, ldd, variant,
+                     epilogue, partition, items_per_group, ws, ws_bytes, stream);
+}
+
+extern "C" int stc_spmm_csr_batched_f32(int batch, int m, int n, int k, const int* rowptr,
+                                        const int* colidx, const float* vals, long long nnz,
+                                        long long val_bstride, const float* B, long long ldb,
+                                        long long b_bstride, float* C, long long ldc, long long c_bstride,
+                                        int variant, int epilogue, const int* partition,
+                                        int items_per_group, void* ws, size_t ws_bytes, void* stream) {
+  if (batch > 65535) return fail(STC_EUNSUPPORTED, "batch > 65535");
+  return spmm_common(batch, m, n, k, rowptr, colidx, vals, nnz, val_bstride, B, ldb, b_bstride, C, ldc,
+                     c_bstride, nullptr, 0, variant, epilogue, partition, items_per_group, ws, ws_bytes,
+                     stream);
+}
+
+extern "C" int stc_spmm_coo_f32(int n_seg, int n, int k, const int* seg_ptr, const int* cols,
+                                const float* vals, long long nnz, const float* B, long long ldb, float* C,
+                                long long ldc, int variant, const int* partition, int items_per_group,
+                                void* ws, size_t ws_bytes, void* stream) {
+  return spmm_common(1, n_seg, n, k, seg_ptr, cols, vals, nnz, 0, B, ldb, 0, C, ldc, 0, nullptr, 0, variant,
+                     STC_EPILOGUE_NONE, partition, items_per_group, ws, ws_bytes, stream);
+}
+
+// ---- COO row segmentation (plan time) ----------------------------------------------
+
+namespace {
+__global__ void exclusive_from_counts_tail(const int* n_seg, int* seg_ptr, long long nnz) {
+  seg_ptr[*n_seg] = (int)nnz;
+}
+}  // namespace
+
+extern "C" size_t stc_coo_segments_temp_bytes(long long nnz) {
+  size_t a = 0, b = 0;
+  cub::DeviceRunLengthEncode::Encode(nullptr, a, (const int*)nullptr, (int*)nullptr, (int*)nullptr,
+                                     (int*)nullptr, (int)nnz);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int*)nullptr, (int*)nullptr, (int)nnz);
+  // counts buffer (nnz ints) + max of the two temporaries, 256-byte aligned pieces
+  const size_t counts = ((size_t)nnz * sizeof(int) + 255) & ~size_t(255);
+  return counts + ((a > b ? a : b) + 255) + 256;
+}
+
+extern "C" int stc_coo_segments(long long nnz, const int* rows, int* seg_rows, int* seg_ptr, int* n_seg_out,
+                                void* temp, size_t temp_bytes, void* stream) {
+  if (nnz < 0 || nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "bad nnz");
+  if (!seg_ptr || !n_seg_out || (nnz && (!rows || !seg_rows))) return fail(STC_EINVAL, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (nnz == 0) {
+    cudaMemsetAsync(n_seg_out, 0, sizeof(int), st);
+    cudaMemsetAsync(seg_ptr, 0, sizeof(int), st);
+    return check_launch("coo_segments(empty)");
+  }
+  const size_t need = stc_coo_segments_temp_bytes(nnz);
+  if (!temp || temp_bytes < need) return fail(STC_EWORKSPACE, "temp %zu < %zu", temp_bytes, need);
+  char* base = static_cast<char*>(temp);
+  base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base) + 255) & ~uintptr_t(255));
+  int* counts = reinterpret_cast<int*>(base);
+  char* tmp = base + (((size_t)nnz * sizeof(int) + 255) & ~size_t(255));
+  size_t tmp_bytes = temp_bytes - (size_t)(tmp - static_cast<char*>(temp));
+  cudaError_t e = cub::DeviceRunLengthEncode::Encode(tmp, tmp_bytes, rows, seg_rows, counts, n_seg_out,
+                                                     (int)nnz, st);
+  if (e != cudaSuccess) return fail(STC_ELAUNCH, "run-length encode: %s", cudaGetErrorString(e));
+  tmp_bytes = temp_bytes - (size_t)(tmp - static_cast<char*>(temp));
+  // exclusive sum over all nnz slots; slots past n_seg hold garbage counts but
+  // seg_ptr[n_seg] is overwritten with nnz below and later slots are unused.
+  e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, seg_ptr, (int)nnz, st);
+  if (e != cudaSuccess) return fail(STC_ELAUNCH, "exclusive scan: %s", cudaGetErrorString(e));
+  exclusive_from_counts_tail<<<1, 1, 0, st>>>(n_seg_out, seg_ptr, nnz);
+  return check_launch("coo_segments");
+}
+
+// ---- MTTKRP ------------------------------------------------------------------------
+
+extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
+                                   const float* vals, long long nnz, const float* B, long long ldb,
+                                   const float* C, long long ldcf, float* M, long long ldm, int variant,
+                                   const int* partition, int items_per_group, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  if (n_seg < 0 || rank < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
+  if (nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "nnz exceeds int32 index range");
+  if (n_seg == 0 || rank == 0) return STC_OK;
+  if (!seg_ptr || !M || (nnz && (!jcrd || !kcrd || !vals || !B || !C))) return fail(STC_EINVAL, "null pointer");
+  if (ldb < rank || ldcf < rank || ldm < rank) return fail(STC_EINVAL, "leading dimension smaller than rank");
+  if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
+    return fail(STC_EUNSUPPORTED, "MTTKRP supports ROW and MERGE");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec4 = rank % 4 == 0 && ldb % 4 == 0 && ldcf % 4 == 0 && ldm % 4 == 0 && aligned16(B) &&
+                    aligned16(C) && aligned16(M);
+  const int vec = vec4 ? 4 : 1;
+  const int subw = choose_subw(rank, vec);
+  SegOut o{n_seg, rank, seg_ptr, M, ldm, nullptr, 0};
+  MergeShape ms{};
+  if (variant == STC_VARIANT_MERGE) {
+    if (!partition || items_per_group < 1) return fail(STC_EINVAL, "MERGE variant needs a partition");
+    const size_t need = merge_ws_bytes(n_seg, nnz, rank, subw, vec, items_per_group, 1);
+    if (ws_bytes < need || (need && !ws)) return fail(STC_EWORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+    const int sw = subw * vec;
+    const long long n_cta = ceil_div(n_groups_for(n_seg, nnz, items_per_group), kThreads / subw);
+    ms.starts = reinterpret_cast<const int2*>(partition);
+    ms.n_groups = (int)n_groups_for(n_seg, nnz, items_per_group);
+    ms.ipg = items_per_group;
+    ms.head_buf = static_cast<float*>(ws);
+    ms.tail_buf = ms.head_buf + ceil_div(rank, sw) * n_cta * sw;
+  }
+  Launch L{variant, 1, st};
+  if (vec4) {
+    MttkrpOp<4> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
+    return dispatch_subw<4, EPI_NONE, false>(subw, o, ms, op, L);
+  }
+  MttkrpOp<1> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
+  return dispatch_subw<1, EPI_NONE, false>(subw, o, ms, op, L);
+}

@@ -1,0 +1,114 @@
+// Shared device helpers for the sparse-contraction kernels (sm_100a).
+//
+// Memory-path conventions used by every kernel in this library:
+//   * index/value streams (rowptr, colidx, values, COO coordinates) are read
+//     exactly once -> ld.global.nc.L1::no_allocate (do not pollute L1 with them)
+//   * the dense operand that is gathered by sparse coordinates is re-read many
+//     times -> ld.global.nc (read-only path, L1-allocating) with an L2
+//     evict_last policy so hub rows stay resident in the 126 MB L2
+//   * outputs are written once -> st.global.cs (streaming, evict-first)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define STC_DEVICE __device__ __forceinline__
+
+namespace stc {
+
+constexpr int kWarp = 32;
+
+STC_DEVICE int ld_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+STC_DEVICE float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+STC_DEVICE uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Gather of a dense-operand vector: read-only path, L1-cached, L2 evict_last.
+STC_DEVICE float4 ld_gather4(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+STC_DEVICE float ld_gather1(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+STC_DEVICE void st_stream4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+STC_DEVICE void st_stream1(float* p, float v) {
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// ---- VEC-wide register fragments ------------------------------------------------
+
+template <int VEC>
+struct Frag;
+
+template <>
+struct Frag<4> {
+  float v[4];
+  STC_DEVICE void zero() { v[0] = v[1] = v[2] = v[3] = 0.f; }
+  STC_DEVICE void load_gather(const float* p, uint64_t pol) {
+    float4 t = ld_gather4(p, pol);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+  STC_DEVICE void load_plain(const float* p) {
+    float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  }
+  STC_DEVICE void store_stream(float* p) const { st_stream4(p, make_float4(v[0], v[1], v[2], v[3])); }
+  STC_DEVICE void store_plain(float* p) const {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
+template <>
+struct Frag<1> {
+  float v[1];
+  STC_DEVICE void zero() { v[0] = 0.f; }
+  STC_DEVICE void load_gather(const float* p, uint64_t pol) { v[0] = ld_gather1(p, pol); }
+  STC_DEVICE void load_plain(const float* p) { v[0] = *p; }
+  STC_DEVICE void store_stream(float* p) const { st_stream1(p, v[0]); }
+  STC_DEVICE void store_plain(float* p) const { *p = v[0]; }
+};
+
+// Epilogues shared by every dense-output kernel: out = act(acc + D).
+enum Epilogue : int { EPI_NONE = 0, EPI_RELU = 1 };
+
+template <int EPI>
+STC_DEVICE float act(float x) {
+  if constexpr (EPI == EPI_RELU) return x > 0.f ? x : 0.f;
+  return x;
+}
+
+// Mask of the SUBW-lane sub-warp that contains this lane.
+template <int SUBW>
+STC_DEVICE unsigned subwarp_mask() {
+  if constexpr (SUBW == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << SUBW) - 1u) << (lane & ~(unsigned)(SUBW - 1));
+  }
+}
+
+}  // namespace stc

@@ -1,0 +1,324 @@
+"""Kernel-level operators on device buffers (thin wrappers over ``libstc.so``).
+
+These are the building blocks the engine's variant dispatch calls; they are
+also usable directly (``spmm_csr(rowptr, colidx, vals, B)`` etc.). Every
+function launches on ``torch.cuda.current_stream()`` and allocates outputs,
+partitions and workspaces with torch (the C ABI never allocates).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi
+from ._abi import check, lib, ptr, require_cuda, stream_handle
+
+# Items (row ends + stored entries) per sub-warp in the merge-path split.
+DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "128"))
+# Row-length skew (max / mean) above which the nnz-balanced split is chosen.
+MERGE_SKEW_THRESHOLD = 8.0
+# Dense widths above which the column-tiled variant is chosen.
+COLTILE_MIN_K = 512
+
+
+def _f32(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype != torch.float32:
+        raise TypeError(f"expected float32, got {t.dtype}")
+    return t
+
+
+def _i32(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype != torch.int32:
+        raise TypeError(f"expected int32 indices, got {t.dtype}")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# Plans (cached per sparse structure, like the reference caches a Schedule)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class RowStats:
+    m: int
+    nnz: int
+    max_row: int
+
+    @property
+    def skew(self) -> float:
+        mean = self.nnz / self.m if self.m else 0.0
+        return self.max_row / mean if mean > 0 else 0.0
+
+
+def row_stats(rowptr: torch.Tensor) -> RowStats:
+    m = rowptr.numel() - 1
+    if m <= 0:
+        return RowStats(max(m, 0), 0, 0)
+    lens = rowptr[1:] - rowptr[:-1]
+    mx, nnz = torch.stack([lens.max().long(), rowptr[-1].long()]).tolist()
+    return RowStats(m, int(nnz), int(mx))
+
+
+def choose_variant(stats: RowStats, k: int, aligned: bool = True) -> str:
+    """The reference's plan for C(i,k)=A(i,j)*B(j,k) is always [i,j,k] with
+    tiles {k} (scheduler.py / tiling.py); on the device the same plan splits
+    into three variants by the shape of the data."""
+    if k >= COLTILE_MIN_K and aligned:
+        return "coltile"
+    if stats.skew > MERGE_SKEW_THRESHOLD or stats.max_row > 4096:
+        return "merge"
+    return "row"
+
+
+@dataclass
+class MergePartition:
+    starts: torch.Tensor      # int32 [2 * (n_groups + 1)]
+    items_per_group: int
+    n_groups: int
+
+
+def merge_partition(rowptr: torch.Tensor, nnz: int,
+                    items_per_group: int = DEFAULT_ITEMS_PER_GROUP) -> MergePartition:
+    require_cuda(rowptr)
+    _i32(rowptr)
+    m = rowptr.numel() - 1
+    groups = int(lib().stc_merge_path_groups(m, nnz, items_per_group))
+    starts = torch.empty(2 * (groups + 1), dtype=torch.int32, device=rowptr.device)
+    rc = lib().stc_merge_path_partition(m, nnz, ptr(rowptr), items_per_group, ptr(starts),
+                                        stream_handle())
+    check(rc, "stc_merge_path_partition")
+    return MergePartition(starts, items_per_group, groups)
+
+
+def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int, batch: int,
+                   device) -> torch.Tensor | None:
+    n = int(lib().stc_spmm_workspace_bytes(m, nnz, k, _abi.VARIANTS[variant], items_per_group, batch))
+    if n == 0:
+        return None
+    return torch.empty((n + 3) // 4, dtype=torch.float32, device=device)
+
+
+# ---------------------------------------------------------------------------
+# SpMM
+# ---------------------------------------------------------------------------
+
+
+def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor,
+             *, out: torch.Tensor | None = None, addend: torch.Tensor | None = None,
+             relu: bool = False, variant: str | None = None,
+             partition: MergePartition | None = None, workspace: torch.Tensor | None = None,
+             stats: RowStats | None = None) -> torch.Tensor:
+    """``C = act(A @ B + addend)`` with A in CSR (int32 rowptr/colidx, fp32 vals)."""
+    require_cuda(rowptr, colidx, vals, B)
+    _i32(rowptr), _i32(colidx), _f32(vals), _f32(B)
+    if B.dim() != 2 or B.stride(1) != 1:
+        raise ValueError("B must be a 2-D row-major (stride(1) == 1) tensor")
+    m = rowptr.numel() - 1
+    n, k = B.shape
+    nnz = vals.numel()
+    if out is None:
+        out = torch.empty((m, k), dtype=torch.float32, device=B.device)
+    if out.shape != (m, k) or out.stride(1) != 1:
+        raise ValueError("out must be an (m, k) row-major tensor")
+    if addend is not None and (addend.shape != (m, k) or addend.stride(1) != 1):
+        raise ValueError("addend must be an (m, k) row-major tensor")
+    if variant is None:
+        stats = stats or row_stats(rowptr)
+        variant = choose_variant(stats, k, aligned=(k % 4 == 0))
+    v = _abi.VARIANTS[variant]
+    ipg = 0
+    if variant == "merge":
+        partition = partition or merge_partition(rowptr, nnz)
+        ipg = partition.items_per_group
+        if workspace is None:
+            workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * 4
+    rc = lib().stc_spmm_csr_f32(
+        m, n, k, ptr(rowptr), ptr(colidx), ptr(vals), nnz, ptr(B), B.stride(0), ptr(out),
+        out.stride(0), ptr(addend), 0 if addend is None else addend.stride(0), v,
+        _abi.EPILOGUE_RELU if relu else _abi.EPILOGUE_NONE,
+        None if partition is None else ptr(partition.starts), ipg, ptr(workspace), ws_bytes,
+        stream_handle())
+    check(rc, "stc_spmm_csr_f32")
+    return out
+
+
+def spmm_csr_batched(rowptr, colidx, vals: torch.Tensor, B: torch.Tensor, *,
+                     out: torch.Tensor | None = None, variant: str | None = None,
+                     partition: MergePartition | None = None,
+                     workspace: torch.Tensor | None = None,
+                     stats: RowStats | None = None) -> torch.Tensor:
+    """Shared-structure batched SpMM: vals [Z, nnz], B [Z, n, k] -> out [Z, m, k]."""
+    require_cuda(rowptr, colidx, vals, B)
+    Z, n, k = B.shape
+    m = rowptr.numel() - 1
+    nnz = colidx.numel()
+    if vals.shape != (Z, nnz) or vals.stride(1) != 1 or B.stride(2) != 1:
+        raise ValueError("vals must be [Z, nnz] and B [Z, n, k] row-major")
+    if out is None:
+        out = torch.empty((Z, m, k), dtype=torch.float32, device=B.device)
+    if variant is None:
+        stats = stats or row_stats(rowptr)
+        variant = "merge" if stats.skew > MERGE_SKEW_THRESHOLD else "row"
+    if variant == "coltile":
+        variant = "row"
+    ipg = 0
+    if variant == "merge":
+        partition = partition or merge_partition(rowptr, nnz)
+        ipg = partition.items_per_group
+        if workspace is None:
+            workspace = spmm_workspace(m, nnz, k, variant, ipg, Z, B.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * 4
+    rc = lib().stc_spmm_csr_batched_f32(
+        Z, m, n, k, ptr(rowptr), ptr(colidx), ptr(vals), nnz, vals.stride(0), ptr(B), B.stride(1),
+        B.stride(0), ptr(out), out.stride(1), out.stride(0), _abi.VARIANTS[variant],
+        _abi.EPILOGUE_NONE, None if partition is None else ptr(partition.starts), ipg,
+        ptr(workspace), ws_bytes, stream_handle())
+    check(rc, "stc_spmm_csr_batched_f32")
+    return out
+
+
+@dataclass
+class Segments:
+    """Distinct-row segmentation of a sorted COO row column."""
+
+    rows: torch.Tensor     # int32 [n_seg]
+    ptr: torch.Tensor      # int32 [n_seg + 1]
+
+    @property
+    def n_seg(self) -> int:
+        return self.rows.numel()
+
+
+def coo_segments(row_crd: torch.Tensor) -> Segments:
+    require_cuda(row_crd)
+    _i32(row_crd)
+    nnz = row_crd.numel()
+    dev = row_crd.device
+    seg_rows = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    seg_ptr = torch.empty(nnz + 1, dtype=torch.int32, device=dev)
+    n_seg = torch.zeros(1, dtype=torch.int32, device=dev)
+    tb = int(lib().stc_coo_segments_temp_bytes(nnz))
+    temp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+    rc = lib().stc_coo_segments(nnz, ptr(row_crd), ptr(seg_rows), ptr(seg_ptr), ptr(n_seg), ptr(temp),
+                                tb, stream_handle())
+    check(rc, "stc_coo_segments")
+    s = int(n_seg.item())
+    return Segments(seg_rows[:s].clone(), seg_ptr[: s + 1].clone())
+
+
+def spmm_segments(seg: Segments, colidx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, *,
+                  variant: str | None = None, partition: MergePartition | None = None,
+                  workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """COO/DCSR SpMM: one output row per segment (the [compressed, dense] output)."""
+    return spmm_csr(seg.ptr, colidx, vals, B, variant=variant, partition=partition,
+                    workspace=workspace)
+
+
+# ---------------------------------------------------------------------------
+# SDDMM / softmax / attention
+# ---------------------------------------------------------------------------
+
+
+def _head_view(X: torch.Tensor, name: str):
+    """(H, rows, d) with unit last stride -> (tensor, head stride, row stride)."""
+    if X.dim() == 2:
+        X = X.unsqueeze(0)
+    if X.dim() != 3 or X.stride(2) != 1:
+        raise ValueError(f"{name} must be [rows, d] or [heads, rows, d] with unit last stride")
+    return X, X.stride(0) if X.shape[0] > 1 else 0, X.stride(1)
+
+
+def sddmm_csr(rowptr, colidx, Q: torch.Tensor, K: torch.Tensor, *, maskvals=None,
+              scale: float = 1.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """``S[h, p] = scale * mask[p] * <Q[h, i], K[h, colidx[p]]>`` -> [H, nnz] (or [nnz])."""
+    require_cuda(rowptr, colidx, Q, K)
+    squeeze = Q.dim() == 2
+    Q3, qhs, qrs = _head_view(_f32(Q), "Q")
+    K3, khs, krs = _head_view(_f32(K), "K")
+    H, m, d = Q3.shape
+    nnz = colidx.numel()
+    if out is None:
+        out = torch.empty((H, nnz), dtype=torch.float32, device=Q.device)
+    rc = lib().stc_sddmm_csr_f32(m, K3.shape[1], d, H, ptr(rowptr), ptr(colidx), ptr(maskvals), nnz,
+                                 ptr(Q3), qhs, qrs, ptr(K3), khs, krs, float(scale), ptr(out),
+                                 stream_handle())
+    check(rc, "stc_sddmm_csr_f32")
+    return out[0] if squeeze else out
+
+
+def segment_softmax_(rowptr: torch.Tensor, vals: torch.Tensor) -> torch.Tensor:
+    """In-place softmax over each row's stored values; vals [nnz] or [H, nnz]."""
+    require_cuda(rowptr, vals)
+    v2 = vals.unsqueeze(0) if vals.dim() == 1 else vals
+    if not v2.is_contiguous():
+        raise ValueError("vals must be contiguous")
+    rc = lib().stc_segsoftmax_csr_f32(rowptr.numel() - 1, v2.shape[0], ptr(rowptr), v2.shape[1], ptr(v2),
+                                      stream_handle())
+    check(rc, "stc_segsoftmax_csr_f32")
+    return vals
+
+
+def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | None = None,
+                     return_probs: bool = False):
+    """Fused ``O = softmax_rows(scale * M .* QK^T) V``; optionally also S and P [H, nnz]."""
+    require_cuda(rowptr, colidx, Q, K, V)
+    squeeze = Q.dim() == 2
+    Q3, qhs, qrs = _head_view(_f32(Q), "Q")
+    K3, khs, krs = _head_view(_f32(K), "K")
+    V3, vhs, vrs = _head_view(_f32(V), "V")
+    H, m, d = Q3.shape
+    nnz = colidx.numel()
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    O = torch.empty((H, m, d), dtype=torch.float32, device=Q.device)
+    S = P = None
+    if return_probs:
+        S = torch.empty((H, nnz), dtype=torch.float32, device=Q.device)
+        P = torch.empty((H, nnz), dtype=torch.float32, device=Q.device)
+    rc = lib().stc_sparse_attention_f32(
+        m, K3.shape[1], d, H, ptr(rowptr), ptr(colidx), ptr(maskvals), nnz, ptr(Q3), qhs, qrs, ptr(K3),
+        khs, krs, ptr(V3), vhs, vrs, float(scale), ptr(O), O.stride(0), O.stride(1), ptr(S), ptr(P),
+        stream_handle())
+    check(rc, "stc_sparse_attention_f32")
+    if squeeze:
+        O = O[0]
+        S = None if S is None else S[0]
+        P = None if P is None else P[0]
+    return (O, S, P) if return_probs else O
+
+
+# ---------------------------------------------------------------------------
+# MTTKRP
+# ---------------------------------------------------------------------------
+
+
+def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tensor, *,
+                variant: str = "merge", partition: MergePartition | None = None,
+                workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """``M[s, :] = sum_{p in segment s} (T[p] * B[j[p], :]) * C[k[p], :]`` -> [n_seg, R]."""
+    require_cuda(jcrd, kcrd, vals, B, C)
+    R = B.shape[1]
+    if C.shape[1] != R or B.stride(1) != 1 or C.stride(1) != 1:
+        raise ValueError("factor matrices must be row-major with the same rank")
+    nnz = vals.numel()
+    n_seg = seg.n_seg
+    M = torch.empty((n_seg, R), dtype=torch.float32, device=B.device)
+    ipg = 0
+    if variant == "merge":
+        partition = partition or merge_partition(seg.ptr, nnz)
+        ipg = partition.items_per_group
+        if workspace is None:
+            workspace = spmm_workspace(n_seg, nnz, R, "merge", ipg, 1, B.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * 4
+    rc = lib().stc_mttkrp_coo3_f32(
+        n_seg, R, ptr(seg.ptr), ptr(jcrd), ptr(kcrd), ptr(vals), nnz, ptr(B), B.stride(0), ptr(C),
+        C.stride(0), ptr(M), M.stride(0), _abi.VARIANTS[variant],
+        None if partition is None else ptr(partition.starts), ipg, ptr(workspace), ws_bytes,
+        stream_handle())
+    check(rc, "stc_mttkrp_coo3_f32")
+    return M

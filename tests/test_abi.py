@@ -1,0 +1,75 @@
+"""The C-ABI library loads without a GPU and exports exactly what include/stc.h declares."""
+
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2405_16883_b200 import _abi, _build
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "stc.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(stc_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    syms = declared_symbols()
+    for s in ["stc_spmm_csr_f32", "stc_spmm_coo_f32", "stc_sddmm_csr_f32", "stc_segsoftmax_csr_f32",
+              "stc_sparse_attention_f32", "stc_mttkrp_coo3_f32", "stc_merge_path_partition",
+              "stc_spmm_workspace_bytes", "stc_last_error", "stc_abi_version"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    if not _build.LIB.exists():
+        _build.build()
+    lib = _abi.load_library()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(_abi.SIGNATURES)
+
+
+def test_host_only_entry_points():
+    lib = _abi.load_library()
+    assert lib.stc_abi_version() == 1
+    assert lib.stc_last_error() == b""
+    assert lib.stc_merge_path_groups(10, 30, 8) == 5
+    assert lib.stc_merge_path_groups(0, 0, 8) == 0
+    assert lib.stc_merge_path_groups(10, 30, 0) == -1
+    assert lib.stc_spmm_workspace_bytes(1000, 5000, 64, _abi.VARIANT_ROW, 128, 1) == 0
+    assert lib.stc_spmm_workspace_bytes(1000, 5000, 64, _abi.VARIANT_MERGE, 128, 1) > 0
+
+
+def test_argument_validation_without_gpu():
+    """Bad arguments are rejected before any launch (negative codes + message)."""
+    lib = _abi.load_library()
+    rc = lib.stc_spmm_csr_f32(-1, 4, 4, None, None, None, 0, None, 4, None, 4, None, 0,
+                              _abi.VARIANT_ROW, 0, None, 0, None, 0, None)
+    assert rc == _abi.STC_EINVAL and b"negative" in lib.stc_last_error()
+    rc = lib.stc_spmm_csr_f32(4, 4, 4, 8, 8, 8, 4, 16, 4, 16, 4, None, 0, 7, 0, None, 0, None, 0, None)
+    assert rc == _abi.STC_EINVAL and b"variant" in lib.stc_last_error()
+    rc = lib.stc_spmm_csr_f32(4, 4, 4, 8, 8, 8, 4, 16, 4, 16, 4, None, 0, _abi.VARIANT_MERGE, 0, None,
+                              128, None, 0, None)
+    assert rc == _abi.STC_EINVAL and b"partition" in lib.stc_last_error()
+    rc = lib.stc_sddmm_csr_f32(4, 4, 48, 1, 8, 8, None, 4, 16, 0, 48, 16, 0, 48, 1.0, 32, None)
+    assert rc == _abi.STC_EUNSUPPORTED
+    with pytest.raises(ValueError):
+        _abi.check(rc, "sddmm")
+
+
+def test_product_path_fails_loudly_without_cuda(monkeypatch):
+    import torch
+
+    import paper_2405_16883_b200 as st
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    A = st.build_from_entries((2, 2), st.csr(2, 2), [((0, 1), 1.0)], name="A", device="cpu")
+    B = st.from_dense([[1.0, 2.0], [3.0, 4.0]], name="B", device="cpu")
+    e = st.parse("C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
+    with pytest.raises(_abi.ExtensionUnavailable):
+        st.run(e)

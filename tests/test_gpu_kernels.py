@@ -1,0 +1,214 @@
+"""Kernel-level parity on the B200: every variant, shape edge cases, determinism.
+
+Checked against the C oracle (float64, reference summation order) with the
+north-star gate: per output row, max |gpu - oracle| <= 1e-5 * max of the
+row's absolute-value contraction (|A| @ |B| etc.).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import native, restate
+from oracle.restate import parity_gate
+from paper_2405_16883_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def make_csr(rng, m, n, lens):
+    lens = np.asarray(lens, dtype=np.int64)
+    lens = np.minimum(lens, n)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    ci = np.concatenate([np.sort(rng.choice(n, int(L), replace=False)) for L in lens]) if m else np.zeros(0)
+    v = rng.uniform(-1, 1, rp[-1]).astype(np.float32)
+    return rp, ci.astype(np.int64), v
+
+
+def dev(rp, ci, v):
+    return (torch.from_numpy(rp).int().cuda(), torch.from_numpy(ci).int().cuda(),
+            torch.from_numpy(v).float().cuda())
+
+
+STRUCTS = {
+    "uniform": lambda r: (300, 200, r.integers(0, 30, 300)),
+    "skewed": lambda r: (400, 500, np.where(np.arange(400) % 97 == 3, 450, r.integers(0, 4, 400))),
+    "one_heavy": lambda r: (5, 6000, [0, 5999, 1, 0, 2]),
+    "empty_rows": lambda r: (64, 50, np.where(np.arange(64) % 3 == 0, 0, 5)),
+    "all_empty": lambda r: (17, 9, np.zeros(17, dtype=np.int64)),
+    "single_row": lambda r: (1, 100, [37]),
+    "trailing_empty": lambda r: (40, 30, np.where(np.arange(40) > 20, 0, 7)),
+}
+
+
+@pytest.mark.parametrize("struct", list(STRUCTS))
+@pytest.mark.parametrize("variant", ["row", "merge", "coltile"])
+@pytest.mark.parametrize("k", [1, 3, 4, 13, 64, 128, 136, 260])
+def test_spmm_variants(struct, variant, k):
+    if variant == "coltile" and k % 4:
+        pytest.skip("coltile needs k % 4 == 0")
+    rng = np.random.default_rng(hash((struct, k)) % 2**32)
+    m, n, lens = STRUCTS[struct](rng)
+    rp, ci, v = make_csr(rng, m, n, lens)
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    want = native.spmm_csr(rp, ci, v, B)
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B))
+    R, Cc, V = dev(rp, ci, v)
+    got = ops.spmm_csr(R, Cc, V, torch.from_numpy(B).cuda(), variant=variant).cpu().numpy()
+    ok, worst = parity_gate(got, want, bound, TOL)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("ipg", [1, 2, 7, 33, 128, 1000])
+@pytest.mark.parametrize("k", [4, 64, 128])
+def test_merge_carries_at_every_granularity(ipg, k):
+    rng = np.random.default_rng(ipg * 100 + k)
+    lens = np.concatenate([[0, 0], rng.integers(0, 6, 200), [3000], rng.integers(0, 3, 100), [0, 800, 0]])
+    m = len(lens)
+    rp, ci, v = make_csr(rng, m, 4000, lens)
+    B = rng.uniform(-1, 1, (4000, k)).astype(np.float32)
+    D = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    R, Cc, V = dev(rp, ci, v)
+    part = ops.merge_partition(R, len(v), ipg)
+    for relu in (False, True):
+        got = ops.spmm_csr(R, Cc, V, torch.from_numpy(B).cuda(), addend=torch.from_numpy(D).cuda(),
+                           relu=relu, variant="merge", partition=part).cpu().numpy()
+        want = native.spmm_csr(rp, ci, v, B, addend=D, relu=relu)
+        bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B), addend=np.abs(D))
+        ok, worst = parity_gate(got, want, bound, TOL)
+        assert ok, (relu, worst)
+
+
+def test_merge_partition_matches_host_search():
+    rng = np.random.default_rng(3)
+    rp, ci, v = make_csr(rng, 500, 100, rng.integers(0, 12, 500))
+    R, _, _ = dev(rp, ci, v)
+    for ipg in (1, 5, 64):
+        part = ops.merge_partition(R, len(v), ipg)
+        st = part.starts.cpu().numpy().reshape(-1, 2)
+        m, nnz = 500, len(v)
+        diags = np.minimum(np.arange(part.n_groups + 1) * ipg, m + nnz)
+        key = rp[1:] + np.arange(1, m + 1)
+        rows = np.searchsorted(key, diags, side="right")
+        assert np.array_equal(st[:, 0], rows)
+        assert np.array_equal(st[:, 1], diags - rows)
+
+
+def test_spmm_deterministic_bitwise():
+    rng = np.random.default_rng(11)
+    lens = np.where(np.arange(2000) % 500 == 1, 20000, rng.integers(0, 10, 2000))
+    rp, ci, v = make_csr(rng, 2000, 30000, lens)
+    B = torch.randn(30000, 128, device="cuda")
+    R, Cc, V = dev(rp, ci, v)
+    a = ops.spmm_csr(R, Cc, V, B, variant="merge")
+    b = ops.spmm_csr(R, Cc, V, B, variant="merge")
+    assert torch.equal(a, b)
+
+
+def test_strided_and_unaligned_operands():
+    rng = np.random.default_rng(12)
+    rp, ci, v = make_csr(rng, 100, 80, rng.integers(0, 10, 100))
+    R, Cc, V = dev(rp, ci, v)
+    big = torch.randn(80, 70, device="cuda")
+    B = big[:, 1:38]  # row stride 70, unaligned start -> scalar path
+    want = native.spmm_csr(rp, ci, v, B.cpu().numpy())
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B.cpu().numpy()))
+    for variant in ("row", "merge"):
+        got = ops.spmm_csr(R, Cc, V, B, variant=variant).cpu().numpy()
+        assert parity_gate(got, want, bound, TOL)[0]
+
+
+def test_batched_spmm():
+    rng = np.random.default_rng(13)
+    rp, ci, v = make_csr(rng, 300, 300, rng.integers(0, 40, 300))
+    Z = 3
+    vals = rng.uniform(0, 1, (Z, len(v))).astype(np.float32)
+    B = rng.standard_normal((Z, 300, 64)).astype(np.float32)
+    R, Cc, _ = dev(rp, ci, v)
+    for variant in ("row", "merge"):
+        got = ops.spmm_csr_batched(R, Cc, torch.from_numpy(vals).cuda(), torch.from_numpy(B).cuda(),
+                                   variant=variant).cpu().numpy()
+        for z in range(Z):
+            want = native.spmm_csr(rp, ci, vals[z], B[z])
+            bound = native.spmm_csr(rp, ci, vals[z], np.abs(B[z]))
+            assert parity_gate(got[z], want, bound, TOL)[0]
+
+
+@pytest.mark.parametrize("d", [4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("heads", [1, 3])
+def test_sddmm(d, heads):
+    rng = np.random.default_rng(d * 10 + heads)
+    rp, ci, mv = make_csr(rng, 120, 90, rng.integers(0, 50, 120))
+    Q = rng.standard_normal((heads, 120, d)).astype(np.float32)
+    K = rng.standard_normal((heads, 90, d)).astype(np.float32)
+    R, Cc, MV = dev(rp, ci, mv)
+    got = ops.sddmm_csr(R, Cc, torch.from_numpy(Q).cuda(), torch.from_numpy(K).cuda(), maskvals=MV,
+                        scale=0.5).cpu().numpy()
+    for h in range(heads):
+        want = 0.5 * native.sddmm_csr(rp, ci, mv, Q[h], K[h])
+        bound = 0.5 * native.sddmm_csr(rp, ci, np.abs(mv), np.abs(Q[h]), np.abs(K[h]))
+        rows = np.repeat(np.arange(120), np.diff(rp))
+        err = np.abs(got[h] - want)
+        lim = np.zeros(120)
+        np.maximum.at(lim, rows, bound)
+        assert np.all(err <= TOL * lim[rows] + 0.0)
+
+
+def test_softmax_and_fused_attention():
+    rng = np.random.default_rng(21)
+    m = n = 200
+    lens = np.minimum(np.arange(m) + 1, 40)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    ci = np.concatenate([np.arange(max(0, q - L + 1), q + 1) for q, L in zip(range(m), lens)])
+    mv = np.ones(len(ci), dtype=np.float32)
+    H, d = 2, 64
+    Q = rng.standard_normal((H, m, d)).astype(np.float32)
+    K = rng.standard_normal((H, n, d)).astype(np.float32)
+    V = rng.standard_normal((H, n, d)).astype(np.float32)
+    R, Cc, MV = dev(rp, ci, mv)
+    Qt, Kt, Vt = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+    O, S, P = ops.sparse_attention(R, Cc, Qt, Kt, Vt, maskvals=MV, scale=0.125, return_probs=True)
+    O2 = ops.sparse_attention(R, Cc, Qt, Kt, Vt, maskvals=MV, scale=0.125)
+    S_u = ops.sddmm_csr(R, Cc, Qt, Kt, maskvals=MV, scale=0.125)
+    P_u = ops.segment_softmax_(R, S_u.clone())
+    O_u = ops.spmm_csr_batched(R, Cc, P_u.contiguous(), Vt)
+    for h in range(H):
+        s_ref = 0.125 * native.sddmm_csr(rp, ci, mv, Q[h], K[h])
+        p_ref = native.segment_softmax(rp, s_ref)
+        o_ref = native.spmm_csr(rp, ci, p_ref, V[h])
+        o_bound = native.spmm_csr(rp, ci, p_ref, np.abs(V[h]))
+        s_bound = 0.125 * native.sddmm_csr(rp, ci, mv, np.abs(Q[h]), np.abs(K[h]))
+        assert np.all(np.abs(S[h].cpu().numpy() - s_ref) <= TOL * s_bound + 1e-12)
+        assert np.abs(P[h].cpu().numpy() - p_ref).max() <= TOL
+        assert np.abs(P_u[h].cpu().numpy() - p_ref).max() <= TOL
+        for o in (O[h], O2[h], O_u[h]):
+            assert parity_gate(o.cpu().numpy(), o_ref, o_bound, TOL)[0]
+
+
+def test_coo_segments_and_mttkrp():
+    rng = np.random.default_rng(31)
+    dim = 300
+    i = np.sort(np.minimum(rng.zipf(1.3, 5000) - 1, dim - 1))
+    j = rng.integers(0, dim, 5000)
+    k = rng.integers(0, dim, 5000)
+    key = np.unique((i * dim + j) * dim + k)
+    i, j, k = key // (dim * dim), (key // dim) % dim, key % dim
+    vals = rng.uniform(0, 1, len(key)).astype(np.float32)
+    B = rng.uniform(0, 1, (dim, 32)).astype(np.float32)
+    C = rng.uniform(0, 1, (dim, 32)).astype(np.float32)
+    seg = ops.coo_segments(torch.from_numpy(i).int().cuda())
+    rows_ref, ptr_ref = restate.coo_segments(i)
+    assert np.array_equal(seg.rows.cpu().numpy(), rows_ref)
+    assert np.array_equal(seg.ptr.cpu().numpy(), ptr_ref)
+    Jt, Kt = torch.from_numpy(j).int().cuda(), torch.from_numpy(k).int().cuda()
+    Vt = torch.from_numpy(vals).cuda()
+    want = native.mttkrp(ptr_ref, j, k, vals, B, C)
+    for variant in ("row", "merge"):
+        for R in (32, 7):
+            got = ops.mttkrp_coo3(seg, Jt, Kt, Vt, torch.from_numpy(B[:, :R].copy()).cuda(),
+                                  torch.from_numpy(C[:, :R].copy()).cuda(), variant=variant).cpu().numpy()
+            assert parity_gate(got, want[:, :R], want[:, :R], TOL)[0]
