@@ -133,11 +133,12 @@ int stc_sparse_attention_f32(int m, int n, int d, int heads, const int* rowptr, 
 
 /* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
  * M[s,:] = sum_{p in seg s} (vals[p] * B[j[p],:]) * C[k[p],:]
+ * B has n_j rows, C has n_k rows (each below 2^32 elements: 32-bit gather offsets).
  * Replaces `_run_sparse_output` with the (i,r) Workspace, engine.py:577-644,
  * 71-90, for M(i,r) = T(i,j,k) * B(j,r) * C(k,r).                           */
 int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
-                        const float* vals, long long nnz, const float* B, long long ldb,
-                        const float* C, long long ldcf, float* M, long long ldm, int variant,
+                        const float* vals, long long nnz, int n_j, const float* B, long long ldb,
+                        int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
                         const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                         void* stream);
 

@@ -60,8 +60,8 @@ SIGNATURES = {
     "stc_segsoftmax_csr_f32": (_i, [_i, _i, _p, _ll, _p, _p]),
     "stc_sparse_attention_f32": (_i, [_i, _i, _i, _i, _p, _p, _p, _ll, _p, _ll, _ll, _p, _ll, _ll, _p,
                                       _ll, _ll, _f, _p, _ll, _ll, _p, _p, _p]),
-    "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _p, _ll, _p, _ll, _p, _ll, _i, _p, _i, _p,
-                                 _sz, _p]),
+    "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _i, _p, _i,
+                                 _p, _sz, _p]),
 }
 
 

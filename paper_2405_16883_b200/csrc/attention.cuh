@@ -72,7 +72,6 @@ __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int h = blockIdx.y;
   if (row >= a.m) return;
-  const uint64_t pol = policy_evict_last();
   const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
   const float* Kh = a.K + h * a.k_hs + lane * 4;
   float* out = a.S + h * a.nnz;
@@ -85,7 +84,7 @@ __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
     for (int t = 0; t < G; ++t) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (t < n) kv = ld_gather4(Kh + (long long)c * a.k_rs, pol);
+      if (t < n) kv = ld_gather4(Kh + (long long)c * a.k_rs);
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
     const float s = transpose_reduce<G>(part, lane, mask);
@@ -123,7 +122,6 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int h = blockIdx.y;
   if (row >= a.m) return;
-  const uint64_t pol = policy_evict_last();
   const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
   const float* Kh = a.K + h * a.k_hs + lane * 4;
   const float* Vh = a.V + h * a.v_hs + lane * 4;
@@ -141,8 +139,8 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
       vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (t < n) {
-        kv = ld_gather4(Kh + (long long)c * a.k_rs, pol);
-        vv[t] = ld_gather4(Vh + (long long)c * a.v_rs, pol);
+        kv = ld_gather4(Kh + (long long)c * a.k_rs);
+        vv[t] = ld_gather4(Vh + (long long)c * a.v_rs);
       }
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }

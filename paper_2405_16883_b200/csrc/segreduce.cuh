@@ -31,33 +31,42 @@ namespace stc {
 // Gather ops
 // ---------------------------------------------------------------------------
 
+// Items are staged in a "prepared" form: dense-operand row offsets are
+// pre-multiplied by the leading dimension (32-bit element offsets; the C ABI
+// rejects dense operands of 2^32 elements or more), so a gather is one
+// IMAD.WIDE + one LDG.128. `shift(col0)` moves the dense pointers to the
+// lane's first column once per kernel.
 template <int VEC>
 struct SpmmOp {
   const int* col;     // [nnz]
   const float* val;   // [nnz] (batched: + batch * val_bstride)
   const float* B;     // dense operand, row-major with leading dim ldb
   long long ldb;
+  unsigned lane_off = 0;  // this lane's first column (added in 32-bit)
 
+  static constexpr int kRing = 8;  // gathers in flight per group
   struct Item {
-    int c;
+    unsigned off;
     float v;
   };
+  // The weight is re-read from the staged item at accumulate time (LDS) so the
+  // ring only holds the gathered vectors.
   struct Pre {
     Frag<VEC> b;
-    float v;
   };
-  STC_DEVICE Item load(long long p) const { return Item{ld_stream(col + p), ld_stream(val + p)}; }
+  STC_DEVICE Item load(long long p) const {
+    return Item{(unsigned)((long long)ld_stream(col + p) * ldb), ld_stream(val + p)};
+  }
+  STC_DEVICE static Item dummy() { return Item{0u, 0.f}; }
   template <int SUBW>
   STC_DEVICE Item shfl(const Item& it, int src, unsigned mask) const {
-    return Item{__shfl_sync(mask, it.c, src, SUBW), __shfl_sync(mask, it.v, src, SUBW)};
+    return Item{__shfl_sync(mask, it.off, src, SUBW), __shfl_sync(mask, it.v, src, SUBW)};
   }
-  STC_DEVICE void fetch(const Item& it, int col0, Pre& pre, uint64_t pol) const {
-    pre.b.load_gather(B + (long long)it.c * ldb + col0, pol);
-    pre.v = it.v;
-  }
-  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre) const {
+  STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
+  STC_DEVICE void fetch(const Item& it, Pre& pre) const { pre.b.load_gather(B + (it.off + lane_off)); }
+  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre, const Item& it) const {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(pre.v, pre.b.v[e], acc.v[e]);
+    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v, pre.b.v[e], acc.v[e]);
   }
 };
 
@@ -70,32 +79,36 @@ struct MttkrpOp {
   long long ldb;
   const float* C;
   long long ldcf;
+  unsigned lane_off = 0;
 
-  struct Item {
-    int j, k;
+  static constexpr int kRing = VEC == 4 ? 4 : 8;
+  struct __align__(16) Item {
+    unsigned offb, offc;
     float v;
+    float pad;
   };
   struct Pre {
     Frag<VEC> b, c;
-    float v;
   };
   STC_DEVICE Item load(long long p) const {
-    return Item{ld_stream(jc + p), ld_stream(kc + p), ld_stream(val + p)};
+    return Item{(unsigned)((long long)ld_stream(jc + p) * ldb), (unsigned)((long long)ld_stream(kc + p) * ldcf),
+                ld_stream(val + p), 0.f};
   }
+  STC_DEVICE static Item dummy() { return Item{0u, 0u, 0.f, 0.f}; }
   template <int SUBW>
   STC_DEVICE Item shfl(const Item& it, int src, unsigned mask) const {
-    return Item{__shfl_sync(mask, it.j, src, SUBW), __shfl_sync(mask, it.k, src, SUBW),
-                __shfl_sync(mask, it.v, src, SUBW)};
+    return Item{__shfl_sync(mask, it.offb, src, SUBW), __shfl_sync(mask, it.offc, src, SUBW),
+                __shfl_sync(mask, it.v, src, SUBW), 0.f};
   }
-  STC_DEVICE void fetch(const Item& it, int col0, Pre& pre, uint64_t pol) const {
-    pre.b.load_gather(B + (long long)it.j * ldb + col0, pol);
-    pre.c.load_gather(C + (long long)it.k * ldcf + col0, pol);
-    pre.v = it.v;
+  STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
+  STC_DEVICE void fetch(const Item& it, Pre& pre) const {
+    pre.b.load_gather(B + (it.offb + lane_off));
+    pre.c.load_gather(C + (it.offc + lane_off));
   }
-  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre) const {
+  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre, const Item& it) const {
     // reference term order: (t * B[j,r]) * C[k,r]  (engine.py:394-402)
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(pre.v * pre.b.v[e], pre.c.v[e], acc.v[e]);
+    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v * pre.b.v[e], pre.c.v[e], acc.v[e]);
   }
 };
 
@@ -166,25 +179,58 @@ struct MergeShape {
   long long batch_c_stride;
 };
 
-template <int SUBW, int VEC, int EPI, bool ADD, int U, class Op>
-__global__ void __launch_bounds__(256) merge_kernel(SegOut o, MergeShape ms, Op op) {
+// Staged items / row ends per group: 2048 per CTA, split over its NG groups.
+template <int SUBW>
+__host__ __device__ constexpr int merge_stage_cap() {
+  return 2048 / (256 / SUBW);
+}
+constexpr int kStagePad = 8;  // dummy items after each window: branch-free prefetch
+
+// Dynamic shared memory of merge_kernel (independent of ipg: groups stream
+// their items through a fixed-size window).
+template <int SUBW, int VEC, class Op>
+__host__ __device__ constexpr size_t merge_smem_bytes() {
   constexpr int NG = 256 / SUBW;
   constexpr int SW = SUBW * VEC;
-  __shared__ __align__(16) float Hs[NG][SW];
-  __shared__ __align__(16) float Ts[NG][SW];
-  __shared__ int Hrow[NG], Trow[NG];
+  constexpr int CAP = merge_stage_cap<SUBW>();
+  return (size_t)2 * NG * SW * sizeof(float)               // head / tail partials
+         + (size_t)2 * NG * sizeof(int)                     // their row ids
+         + (size_t)NG * (CAP + kStagePad) * sizeof(typename Op::Item)  // staged items window
+         + (size_t)NG * CAP * sizeof(int);                  // staged row-end window
+}
+
+// One sub-warp ("group") per `ipg` merge items. The group stages a window of
+// its entries' items and of its rows' end offsets in shared memory (coalesced,
+// one round trip per window), then streams the gathers through a U-deep
+// register ring: the gather for entry q+U is issued while entry q is
+// accumulated, independent of row boundaries, so U loads stay in flight
+// across rows.
+template <int SUBW, int VEC, int EPI, bool ADD, int U, bool FULL, class Op>
+__global__ void __launch_bounds__(256, 3) merge_kernel(SegOut o, MergeShape ms, Op op) {
+  static_assert(U <= kStagePad, "ring deeper than the staging pad");
+  using Item = typename Op::Item;
+  constexpr int NG = 256 / SUBW;
+  constexpr int SW = SUBW * VEC;
+  constexpr int CAP = merge_stage_cap<SUBW>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* Hs = reinterpret_cast<float*>(smem_raw);                       // [NG][SW]
+  float* Ts = Hs + NG * SW;                                             // [NG][SW]
+  int* Hrow = reinterpret_cast<int*>(Ts + NG * SW);                     // [NG]
+  int* Trow = Hrow + NG;                                                // [NG]
+  Item* items_all = reinterpret_cast<Item*>(Trow + NG);                 // [NG][CAP]
+  int* rend_all = reinterpret_cast<int*>(items_all + NG * (CAP + kStagePad));  // [NG][CAP]
 
   const int sub = threadIdx.x / SUBW;
   const int lane = threadIdx.x % SUBW;
   const unsigned mask = subwarp_mask<SUBW>();
   const int cta = blockIdx.x;
   const int slab = blockIdx.y;
-  const int z = blockIdx.z;  // batch (head) index; shares the structure
+  const int z = blockIdx.z;
   const int col0 = slab * SW + lane * VEC;
-  const bool col_ok = col0 < o.k;
-  const uint64_t pol = policy_evict_last();
+  const bool col_ok = FULL || col0 < o.k;
+  Item* items = items_all + sub * (CAP + kStagePad);
+  int* rend = rend_all + sub * CAP;
 
-  // batched views
   if (z) {
     op.val += z * ms.batch_val_stride;
     op.B += z * ms.batch_b_stride;
@@ -192,75 +238,94 @@ __global__ void __launch_bounds__(256) merge_kernel(SegOut o, MergeShape ms, Op 
     if constexpr (ADD) o.D += z * ms.batch_c_stride;
   }
   const long long zslab = ((long long)z * gridDim.y + slab) * ms.n_cta;
+  op.shift(col0);
 
   const int g = min(cta * NG + sub, ms.n_groups);
   const int2 s = ms.starts[g];
   const int2 e = ms.starts[min(g + 1, ms.n_groups)];
   const int row0 = s.x;
-  const int row_stop = e.x;   // rows [row0, row_stop) end inside this group
-  const int p_end = e.y;
+  const int n_rows = e.x - s.x;   // rows whose end item this group owns
+  const int n_nnz = e.y - s.y;    // entries this group accumulates
 
-  int row = row0;
-  int cur_start = (row < o.m) ? o.rowptr[row] : s.y;
-  const bool head_mid = (row < o.m) && (s.y > cur_start);
-
-  int rows_base = row;
-  int re_lane = (rows_base + lane < row_stop) ? ld_stream(o.rowptr + rows_base + lane + 1) : INT_MAX;
-  int cur_end = __shfl_sync(mask, re_lane, 0, SUBW);
-
-  Frag<VEC> acc;
-  acc.zero();
+  // row ends of rows [row0 + rb, row0 + rb + CAP), relative to s.y
+  int rb = 0;
+  auto stage_rows = [&](int base) {
+    __syncwarp(mask);
+    for (int t = lane; t < CAP && base + t < n_rows; t += SUBW)
+      rend[t] = ld_stream(o.rowptr + row0 + base + 1 + t) - s.y;
+    __syncwarp(mask);
+  };
+  stage_rows(0);
+  int first_start = 0;
   if (lane == 0) {
+    first_start = (row0 < o.m) ? o.rowptr[row0] : s.y;
     Hrow[sub] = -1;
     Trow[sub] = -1;
   }
-  __syncwarp(mask);
+  first_start = __shfl_sync(mask, first_start, 0, SUBW);
+  const bool head_mid = (row0 < o.m) && (s.y > first_start);
 
-  auto flush_and_advance = [&]() {
-    if (row == row0 && head_mid) {
-      if (col_ok) acc.store_plain(&Hs[sub][lane * VEC]);
+  int r = 0;                                        // current row = row0 + r
+  int cur_end = n_rows > 0 ? rend[0] : INT_MAX;      // relative end of the current row
+  int cur_start = first_start - s.y;                 // relative start (may be negative)
+  Frag<VEC> acc;
+  acc.zero();
+
+  auto flush = [&]() {
+    const int row = row0 + r;
+    if (r == 0 && head_mid) {
+      if (col_ok) acc.store_plain(&Hs[sub * SW + lane * VEC]);
       if (lane == 0) Hrow[sub] = row;
     } else if (col_ok) {
       write_row<VEC, EPI, ADD>(o, row, col0, acc);
     }
     acc.zero();
-    ++row;
+    ++r;
     cur_start = cur_end;
-    if (row - rows_base == SUBW) {
-      rows_base = row;
-      re_lane = (rows_base + lane < row_stop) ? ld_stream(o.rowptr + rows_base + lane + 1) : INT_MAX;
+    if (r - rb == CAP) {
+      rb = r;
+      stage_rows(rb);
     }
-    cur_end = __shfl_sync(mask, re_lane, row - rows_base, SUBW);
+    cur_end = r < n_rows ? rend[r - rb] : INT_MAX;
   };
 
-  for (int base = s.y; base < p_end; base += SUBW) {
-    typename Op::Item it{};
-    if (base + lane < p_end) it = op.load(base + lane);
-    const int n = min(SUBW, p_end - base);
-    for (int q0 = 0; q0 < n; q0 += U) {
-      typename Op::Pre pre[U];
+  typename Op::Pre ring[U];
+  for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
+    const int wn = min(CAP, n_nnz - w0);
+    __syncwarp(mask);
+    for (int t = lane; t < wn + kStagePad; t += SUBW) items[t] = t < wn ? op.load(s.y + w0 + t) : Op::dummy();
+    __syncwarp(mask);
+    int end_w = cur_end - w0;  // current row's end, relative to the window
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (col_ok) op.fetch(items[u], ring[u]);
+    int q0 = 0;
+    for (; q0 + U <= wn; q0 += U) {  // full ring turns: no bounds predicates
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int q = q0 + u;
-        typename Op::Item iu = op.template shfl<SUBW>(it, q & (SUBW - 1), mask);
-        if (q < n && col_ok) op.fetch(iu, col0, pre[u], pol);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = q0 + u;
-        if (q < n) {
-          const int pp = base + q;
-          while (pp >= cur_end) flush_and_advance();
-          op.accumulate(acc, pre[u]);
+        while (q0 + u >= end_w) {
+          flush();
+          end_w = cur_end - w0;
         }
+        op.accumulate(acc, ring[u], items[q0 + u]);
+        if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // remainder of the window
+      if (q0 + u < wn) {
+        while (q0 + u >= end_w) {
+          flush();
+          end_w = cur_end - w0;
+        }
+        op.accumulate(acc, ring[u], items[q0 + u]);
       }
     }
   }
-  while (row < row_stop) flush_and_advance();
-  // tail: the row still open at the end of this group's items
-  if (row < o.m && p_end > cur_start && row == row_stop) {
-    if (col_ok) acc.store_plain(&Ts[sub][lane * VEC]);
-    if (lane == 0) Trow[sub] = row;
+  while (r < n_rows) flush();
+  if (row0 + r < o.m && n_nnz > cur_start && r == n_rows) {
+    if (col_ok) acc.store_plain(&Ts[sub * SW + lane * VEC]);
+    if (lane == 0) Trow[sub] = row0 + r;
   }
   __syncthreads();
 
@@ -268,44 +333,40 @@ __global__ void __launch_bounds__(256) merge_kernel(SegOut o, MergeShape ms, Op 
   const int2 cs = ms.starts[min(cta * NG, ms.n_groups)];
   const bool cta_head_mid = (cs.x < o.m) && (cs.y > o.rowptr[cs.x]);
   const int hr = Hrow[sub];
-  if (hr >= 0) {
+  if (hr >= 0 && col_ok) {
     int lo = sub;
     while (lo > 0 && Trow[lo - 1] == hr) --lo;
     Frag<VEC> sum;
     sum.zero();
-    if (col_ok) {
-      for (int t = lo; t < sub; ++t) {
-        Frag<VEC> part;
-        part.load_plain(&Ts[t][lane * VEC]);
+    for (int t = lo; t < sub; ++t) {
+      Frag<VEC> part;
+      part.load_plain(&Ts[t * SW + lane * VEC]);
 #pragma unroll
-        for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
-      }
-      Frag<VEC> h;
-      h.load_plain(&Hs[sub][lane * VEC]);
+      for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
+    }
+    Frag<VEC> h;
+    h.load_plain(&Hs[sub * SW + lane * VEC]);
 #pragma unroll
-      for (int x = 0; x < VEC; ++x) sum.v[x] += h.v[x];
-      if (lo == 0 && cta_head_mid && hr == cs.x) {
-        sum.store_plain(ms.head_buf + (zslab + cta) * SW + lane * VEC);  // needs earlier CTAs
-      } else {
-        write_row<VEC, EPI, ADD>(o, hr, col0, sum);
-      }
+    for (int x = 0; x < VEC; ++x) sum.v[x] += h.v[x];
+    if (lo == 0 && cta_head_mid && hr == cs.x) {
+      sum.store_plain(ms.head_buf + (zslab + cta) * SW + lane * VEC);  // needs earlier CTAs
+    } else {
+      write_row<VEC, EPI, ADD>(o, hr, col0, sum);
     }
   }
-  if (sub == NG - 1 && Trow[sub] >= 0) {
+  if (sub == NG - 1 && Trow[sub] >= 0 && col_ok) {
     const int tr = Trow[sub];
     int lo = sub;
     while (lo > 0 && Trow[lo - 1] == tr && Hrow[lo] < 0) --lo;
-    if (col_ok) {
-      Frag<VEC> sum;
-      sum.zero();
-      for (int t = lo; t <= sub; ++t) {
-        Frag<VEC> part;
-        part.load_plain(&Ts[t][lane * VEC]);
+    Frag<VEC> sum;
+    sum.zero();
+    for (int t = lo; t <= sub; ++t) {
+      Frag<VEC> part;
+      part.load_plain(&Ts[t * SW + lane * VEC]);
 #pragma unroll
-        for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
-      }
-      sum.store_plain(ms.tail_buf + (zslab + cta) * SW + lane * VEC);
+      for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
     }
+    sum.store_plain(ms.tail_buf + (zslab + cta) * SW + lane * VEC);
   }
 }
 
@@ -378,13 +439,13 @@ __global__ void __launch_bounds__(256) row_kernel(SegOut o, MergeShape ms, Op op
   if (row >= o.m) return;
   const int col0 = slab * SW + lane * VEC;
   const bool col_ok = col0 < o.k;
-  const uint64_t pol = policy_evict_last();
   if (z) {
     op.val += z * ms.batch_val_stride;
     op.B += z * ms.batch_b_stride;
     o.C += z * ms.batch_c_stride;
     if constexpr (ADD) o.D += z * ms.batch_c_stride;
   }
+  op.shift(col0);
   const int start = o.rowptr[row];
   const int end = o.rowptr[row + 1];
   Frag<VEC> acc;
@@ -395,14 +456,15 @@ __global__ void __launch_bounds__(256) row_kernel(SegOut o, MergeShape ms, Op op
     const int n = min(SUBW, end - base);
     for (int q0 = 0; q0 < n; q0 += U) {
       typename Op::Pre pre[U];
+      typename Op::Item iu[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        typename Op::Item iu = op.template shfl<SUBW>(it, (q0 + u) & (SUBW - 1), mask);
-        if (q0 + u < n && col_ok) op.fetch(iu, col0, pre[u], pol);
+        iu[u] = op.template shfl<SUBW>(it, (q0 + u) & (SUBW - 1), mask);
+        if (q0 + u < n && col_ok) op.fetch(iu[u], pre[u]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (q0 + u < n) op.accumulate(acc, pre[u]);
+        if (q0 + u < n) op.accumulate(acc, pre[u], iu[u]);
     }
   }
   if (col_ok) write_row<VEC, EPI, ADD>(o, row, col0, acc);

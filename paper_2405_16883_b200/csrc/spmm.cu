@@ -13,6 +13,7 @@ using namespace stc;
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxIpg = 1024;  // staged items per group (shared memory bound)
 
 int choose_subw(int k, int vec) {
   for (int s : {4, 8, 16}) {
@@ -41,7 +42,7 @@ struct Launch {
 template <int SUBW, int VEC, int EPI, bool ADD, class Op>
 int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
   constexpr int SW = SUBW * VEC;
-  constexpr int U = SUBW >= 8 ? 8 : 4;
+  constexpr int U = SUBW >= 8 ? Op::kRing : 4;
   const int slabs = (int)ceil_div(o.k, SW);
   if (o.m == 0 || slabs == 0) return STC_OK;
   if (L.variant == STC_VARIANT_ROW) {
@@ -53,7 +54,19 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
   ms.n_cta = (int)ceil_div(ms.n_groups, NG);
   if (ms.n_cta == 0) return STC_OK;
   const dim3 grid(ms.n_cta, slabs, L.batch);
-  merge_kernel<SUBW, VEC, EPI, ADD, U, Op><<<grid, kThreads, 0, L.stream>>>(o, ms, op);
+  constexpr size_t smem = merge_smem_bytes<SUBW, VEC, Op>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  if (o.k % SW == 0)
+    merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op><<<grid, kThreads, smem, L.stream>>>(o, ms, op);
+  else
+    merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op><<<grid, kThreads, smem, L.stream>>>(o, ms, op);
   int rc = check_launch("merge_kernel");
   if (rc || ms.n_cta < 2) return rc;
   const dim3 fgrid((unsigned)ceil_div((long long)(ms.n_cta - 1) * SUBW, kThreads), slabs, L.batch);
@@ -110,6 +123,8 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
   if (ldb < k || ldc < k || (D && ldd < k)) return fail(STC_EINVAL, "leading dimension smaller than k");
   if (epilogue != STC_EPILOGUE_NONE && epilogue != STC_EPILOGUE_RELU)
     return fail(STC_EINVAL, "unknown epilogue %d", epilogue);
+  if ((long long)(n + 1) * ldb >= (1LL << 32))
+    return fail(STC_EUNSUPPORTED, "dense operand of 2^32 elements or more (32-bit gather offsets)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec4 = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C) &&
                     (!D || (ldd % 4 == 0 && aligned16(D))) && (val_bs % 4 == 0 || batch == 1) &&
@@ -134,7 +149,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
   ms.batch_c_stride = c_bs;
   if (variant == STC_VARIANT_MERGE) {
     if (!partition) return fail(STC_EINVAL, "MERGE variant needs a partition");
-    if (ipg < 1) return fail(STC_EINVAL, "items_per_group must be >= 1");
+    if (ipg < 1 || ipg > kMaxIpg) return fail(STC_EINVAL, "items_per_group must be in [1, %d]", kMaxIpg);
     const int vec = vec4 ? 4 : 1;
     const size_t need = merge_ws_bytes(m, nnz, k, choose_subw(k, vec), vec, ipg, batch);
     if (ws_bytes < need || (need && !ws))
@@ -264,8 +279,8 @@ extern "C" int stc_coo_segments(long long nnz, const int* rows, int* seg_rows, i
 // ---- MTTKRP ------------------------------------------------------------------------
 
 extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
-                                   const float* vals, long long nnz, const float* B, long long ldb,
-                                   const float* C, long long ldcf, float* M, long long ldm, int variant,
+                                   const float* vals, long long nnz, int n_j, const float* B, long long ldb,
+                                   int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
                                    const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                                    void* stream) {
   if (n_seg < 0 || rank < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
@@ -275,6 +290,9 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   if (ldb < rank || ldcf < rank || ldm < rank) return fail(STC_EINVAL, "leading dimension smaller than rank");
   if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
     return fail(STC_EUNSUPPORTED, "MTTKRP supports ROW and MERGE");
+  if (n_j < 0 || n_k < 0) return fail(STC_EINVAL, "negative factor extent");
+  if ((long long)(n_j + 1) * ldb >= (1LL << 32) || (long long)(n_k + 1) * ldcf >= (1LL << 32))
+    return fail(STC_EUNSUPPORTED, "factor matrix of 2^32 elements or more (32-bit gather offsets)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec4 = rank % 4 == 0 && ldb % 4 == 0 && ldcf % 4 == 0 && ldm % 4 == 0 && aligned16(B) &&
                     aligned16(C) && aligned16(M);
@@ -283,7 +301,8 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   SegOut o{n_seg, rank, seg_ptr, M, ldm, nullptr, 0};
   MergeShape ms{};
   if (variant == STC_VARIANT_MERGE) {
-    if (!partition || items_per_group < 1) return fail(STC_EINVAL, "MERGE variant needs a partition");
+    if (!partition || items_per_group < 1 || items_per_group > kMaxIpg)
+      return fail(STC_EINVAL, "MERGE variant needs a partition with 1 <= items_per_group <= %d", kMaxIpg);
     const size_t need = merge_ws_bytes(n_seg, nnz, rank, subw, vec, items_per_group, 1);
     if (ws_bytes < need || (need && !ws)) return fail(STC_EWORKSPACE, "workspace %zu < %zu", ws_bytes, need);
     const int sw = subw * vec;

@@ -4,8 +4,7 @@
 //   * index/value streams (rowptr, colidx, values, COO coordinates) are read
 //     exactly once -> ld.global.nc.L1::no_allocate (do not pollute L1 with them)
 //   * the dense operand that is gathered by sparse coordinates is re-read many
-//     times -> ld.global.nc (read-only path, L1-allocating) with an L2
-//     evict_last policy so hub rows stay resident in the 126 MB L2
+//     times -> ld.global.nc (read-only path, L1-allocating)
 //   * outputs are written once -> st.global.cs (streaming, evict-first)
 #pragma once
 
@@ -35,19 +34,9 @@ STC_DEVICE uint64_t policy_evict_last() {
   return pol;
 }
 
-// Gather of a dense-operand vector: read-only path, L1-cached, L2 evict_last.
-STC_DEVICE float4 ld_gather4(const float* p, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-STC_DEVICE float ld_gather1(const float* p, uint64_t pol) {
-  float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-  return v;
-}
+// Gather of a dense-operand vector: read-only (non-coherent) path, L1-cached.
+STC_DEVICE float4 ld_gather4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+STC_DEVICE float ld_gather1(const float* p) { return __ldg(p); }
 
 STC_DEVICE void st_stream4(float* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
@@ -67,8 +56,8 @@ template <>
 struct Frag<4> {
   float v[4];
   STC_DEVICE void zero() { v[0] = v[1] = v[2] = v[3] = 0.f; }
-  STC_DEVICE void load_gather(const float* p, uint64_t pol) {
-    float4 t = ld_gather4(p, pol);
+  STC_DEVICE void load_gather(const float* p) {
+    float4 t = ld_gather4(p);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   }
   STC_DEVICE void load_plain(const float* p) {
@@ -85,7 +74,7 @@ template <>
 struct Frag<1> {
   float v[1];
   STC_DEVICE void zero() { v[0] = 0.f; }
-  STC_DEVICE void load_gather(const float* p, uint64_t pol) { v[0] = ld_gather1(p, pol); }
+  STC_DEVICE void load_gather(const float* p) { v[0] = ld_gather1(p); }
   STC_DEVICE void load_plain(const float* p) { v[0] = *p; }
   STC_DEVICE void store_stream(float* p) const { st_stream1(p, v[0]); }
   STC_DEVICE void store_plain(float* p) const { *p = v[0]; }

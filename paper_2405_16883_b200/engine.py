@@ -571,8 +571,12 @@ def _exec_sddmm(ctx: _Ctx, s: _SddmmTerm) -> Tensor:
     Qd = _dense_torch(ctx.t(s.Q), tuple(s.Q.indices.index(v) for v in hs + (s.i, s.d)))
     Kd = _dense_torch(ctx.t(s.K), tuple(s.K.indices.index(v) for v in hs + (s.j, s.d)))
     d = Qd.shape[-1]
-    if d not in (4, 8, 16, 32, 64, 128):
-        raise UnsupportedExpressionError(f"SDDMM head dim {d} (supported: 4..128, powers of two)")
+    dk = next((w for w in (4, 8, 16, 32, 64, 128) if w >= d), None)
+    if dk is None:
+        raise UnsupportedExpressionError(f"SDDMM reduction extent {d} > 128")
+    if dk != d:  # zero-pad the reduction dim to the kernel's lane width (exact: adds 0 products)
+        Qd = torch.nn.functional.pad(Qd, (0, dk - d))
+        Kd = torch.nn.functional.pad(Kd, (0, dk - d))
     vals = ops.sddmm_csr(view.rowptr, view.cols, Qd, Kd, maskvals=view.vals, scale=1.0)
     ctx.chosen.append(f"sddmm:{view.kind}")
     nnz = view.vals.numel()

@@ -316,8 +316,8 @@ def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tenso
             workspace = spmm_workspace(n_seg, nnz, R, "merge", ipg, 1, B.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_mttkrp_coo3_f32(
-        n_seg, R, ptr(seg.ptr), ptr(jcrd), ptr(kcrd), ptr(vals), nnz, ptr(B), B.stride(0), ptr(C),
-        C.stride(0), ptr(M), M.stride(0), _abi.VARIANTS[variant],
+        n_seg, R, ptr(seg.ptr), ptr(jcrd), ptr(kcrd), ptr(vals), nnz, B.shape[0], ptr(B), B.stride(0),
+        C.shape[0], ptr(C), C.stride(0), ptr(M), M.stride(0), _abi.VARIANTS[variant],
         None if partition is None else ptr(partition.starts), ipg, ptr(workspace), ws_bytes,
         stream_handle())
     check(rc, "stc_mttkrp_coo3_f32")
