@@ -46,6 +46,8 @@ SIGNATURES = {
     "stc_abi_version": (_i, []),
     "stc_last_error": (ctypes.c_char_p, []),
     "stc_launch_count": (_ll, []),
+    "stc_l2_set_persisting": (_ll, [_sz]),
+    "stc_l2_reset_persisting": (_i, []),
     "stc_merge_path_groups": (_ll, [_i, _ll, _i]),
     "stc_merge_path_partition": (_i, [_i, _ll, _p, _i, _p, _p]),
     "stc_spmm_workspace_bytes": (_sz, [_i, _ll, _i, _i, _i, _i]),

@@ -37,6 +37,8 @@ struct Launch {
   int variant;
   int batch;
   cudaStream_t stream;
+  const void* window;      // gathered dense operand (L2 access-policy window)
+  size_t window_bytes;
 };
 
 template <int SUBW, int VEC, int EPI, bool ADD, class Op>
@@ -47,7 +49,8 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
   if (o.m == 0 || slabs == 0) return STC_OK;
   if (L.variant == STC_VARIANT_ROW) {
     const dim3 grid((unsigned)ceil_div((long long)o.m * SUBW, kThreads), slabs, L.batch);
-    row_kernel<SUBW, VEC, EPI, ADD, U, Op><<<grid, kThreads, 0, L.stream>>>(o, ms, op);
+    launch_windowed(row_kernel<SUBW, VEC, EPI, ADD, U, Op>, grid, dim3(kThreads), 0, L.stream, L.window,
+                    L.window_bytes, o, ms, op);
     return check_launch("row_kernel");
   }
   constexpr int NG = kThreads / SUBW;
@@ -64,9 +67,11 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
     configured = true;
   }
   if (o.k % SW == 0)
-    merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op><<<grid, kThreads, smem, L.stream>>>(o, ms, op);
+    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op>, grid, dim3(kThreads), smem, L.stream,
+                    L.window, L.window_bytes, o, ms, op);
   else
-    merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op><<<grid, kThreads, smem, L.stream>>>(o, ms, op);
+    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>, grid, dim3(kThreads), smem, L.stream,
+                    L.window, L.window_bytes, o, ms, op);
   int rc = check_launch("merge_kernel");
   if (rc || ms.n_cta < 2) return rc;
   const dim3 fgrid((unsigned)ceil_div((long long)(ms.n_cta - 1) * SUBW, kThreads), slabs, L.batch);
@@ -163,7 +168,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
     ms.head_buf = static_cast<float*>(ws);
     ms.tail_buf = ms.head_buf + (long long)batch * slabs * n_cta * sw;
   }
-  Launch L{variant, batch, st};
+  Launch L{variant, batch, st, B, (size_t)((long long)n * ldb * (batch > 1 && b_bs ? batch : 1)) * sizeof(float)};
   if (vec4) {
     SpmmOp<4> op{colidx, vals, B, ldb};
     return dispatch_spmm<4>(epilogue, D != nullptr, o, ms, op, L);
@@ -313,7 +318,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
     ms.head_buf = static_cast<float*>(ws);
     ms.tail_buf = ms.head_buf + ceil_div(rank, sw) * n_cta * sw;
   }
-  Launch L{variant, 1, st};
+  Launch L{variant, 1, st, B, (size_t)((long long)n_j * ldb) * sizeof(float)};
   if (vec4) {
     MttkrpOp<4> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
     return dispatch_subw<4, EPI_NONE, false>(subw, o, ms, op, L);

@@ -18,7 +18,7 @@ from . import _abi
 from ._abi import check, lib, ptr, require_cuda, stream_handle
 
 # Items (row ends + stored entries) per sub-warp in the merge-path split.
-DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "128"))
+DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "256"))
 # Row-length skew (max / mean) above which the nnz-balanced split is chosen.
 MERGE_SKEW_THRESHOLD = 8.0
 # Dense widths above which the column-tiled variant is chosen.
@@ -72,6 +72,23 @@ def choose_variant(stats: RowStats, k: int, aligned: bool = True) -> str:
     if stats.skew > MERGE_SKEW_THRESHOLD or stats.max_row > 4096:
         return "merge"
     return "row"
+
+
+def l2_set_persisting(nbytes: int) -> int:
+    """Carve out ``nbytes`` of L2 for persisting accesses (device-wide); SpMM-family
+    launches then pin their gathered dense operand there. Returns bytes granted."""
+    if not torch.cuda.is_available():
+        raise _abi.ExtensionUnavailable("no CUDA device")
+    torch.cuda.current_device()
+    got = int(lib().stc_l2_set_persisting(int(nbytes)))
+    if got < 0:
+        check(got, "stc_l2_set_persisting")
+    return got
+
+
+def l2_reset_persisting() -> None:
+    """Demote all persisting L2 lines to normal (call before flushing L2)."""
+    check(lib().stc_l2_reset_persisting(), "stc_l2_reset_persisting")
 
 
 @dataclass

@@ -18,6 +18,7 @@ flush = torch.empty(128 * 1024 * 1024, device="cuda")
 byts = 4 * (A.shape[0] + 1) + 8 * A.nnz + 2 * 4 * A.shape[0] * 128
 
 
+PERSIST = [a for a in sys.argv if a.startswith("persist=")]
 NOFLUSH = "noflush" in sys.argv
 sys.argv = [a for a in sys.argv if a != "noflush"]
 
@@ -26,6 +27,8 @@ def timeit(fn, reps=30):
     ts = []
     for _ in range(reps):
         if not NOFLUSH:
+            if PERSIST:
+                ops.l2_reset_persisting()
             flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -36,6 +39,10 @@ def timeit(fn, reps=30):
     return statistics.median(ts)
 
 
+sys.argv = [a for a in sys.argv if not a.startswith("persist=")]
+if PERSIST:
+    got = ops.l2_set_persisting(int(float(PERSIST[0].split("=")[1]) * 2**20))
+    print("persisting L2 carve-out:", got / 2**20, "MiB")
 for ipg in [int(x) for x in (sys.argv[1:] or ["32", "64", "128", "256", "512"])]:
     part = ops.merge_partition(R, A.nnz, ipg)
     ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", ipg, 1, "cuda")
