@@ -194,8 +194,9 @@ class GCN(Workload):
         torch.backends.cudnn.allow_tf32 = False
         self.stats = ops.row_stats(self.rowptr)
         self.variant = variant or ops.choose_variant(self.stats, self.k)
-        self.ipg = ipg or ops.DEFAULT_ITEMS_PER_GROUP
-        self.partition = ops.merge_partition(self.rowptr, self.nnz, self.ipg) if self.variant == "merge" else None
+        self.partition = ops.merge_partition(self.rowptr, self.nnz, ipg, k=self.k) \
+            if self.variant == "merge" else None
+        self.ipg = self.partition.items_per_group if self.partition else None
         self.ws = ops.spmm_workspace(self.n, self.nnz, self.k, self.variant, self.ipg, 1, device) \
             if self.variant == "merge" else None
         self.Z1 = self.X @ self.W1

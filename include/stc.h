@@ -74,6 +74,12 @@ long long stc_merge_path_groups(int m, long long nnz, int items_per_group);
 int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
                              int* starts, void* stream);
 
+/* Plan-time choice of items_per_group for the MERGE variant: the merged
+ * sequence is cut into exactly enough groups to fill whole waves of resident
+ * CTAs on this device (one wave when a group's staging window allows), so no
+ * partial last wave idles SMs. `kind` 0 = SpMM, 1 = MTTKRP.                  */
+int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind);
+
 /* Workspace for the MERGE variant (carry buffers); 0 for ROW/COLTILE.        */
 size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int items_per_group,
                                 int batch);

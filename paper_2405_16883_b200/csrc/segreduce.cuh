@@ -179,10 +179,15 @@ struct MergeShape {
   long long batch_c_stride;
 };
 
-// Staged items / row ends per group: 2048 per CTA, split over its NG groups.
-template <int SUBW>
+// Staging budget per CTA: 32 KB of items split over its NG groups (CAP items
+// per group), plus CAP/4 row ends per group (restaged when a group owns more rows).
+template <int SUBW, class Op>
 __host__ __device__ constexpr int merge_stage_cap() {
-  return 2048 / (256 / SUBW);
+  return 32768 / ((256 / SUBW) * (int)sizeof(typename Op::Item));
+}
+template <int SUBW, class Op>
+__host__ __device__ constexpr int merge_rows_cap() {
+  return merge_stage_cap<SUBW, Op>() / 4 < 32 ? 32 : merge_stage_cap<SUBW, Op>() / 4;
 }
 constexpr int kStagePad = 8;  // dummy items after each window: branch-free prefetch
 
@@ -192,11 +197,12 @@ template <int SUBW, int VEC, class Op>
 __host__ __device__ constexpr size_t merge_smem_bytes() {
   constexpr int NG = 256 / SUBW;
   constexpr int SW = SUBW * VEC;
-  constexpr int CAP = merge_stage_cap<SUBW>();
+  constexpr int CAP = merge_stage_cap<SUBW, Op>();
+  constexpr int CAPR = merge_rows_cap<SUBW, Op>();
   return (size_t)2 * NG * SW * sizeof(float)               // head / tail partials
          + (size_t)2 * NG * sizeof(int)                     // their row ids
          + (size_t)NG * (CAP + kStagePad) * sizeof(typename Op::Item)  // staged items window
-         + (size_t)NG * CAP * sizeof(int);                  // staged row-end window
+         + (size_t)NG * CAPR * sizeof(int);                 // staged row-end window
 }
 
 // One sub-warp ("group") per `ipg` merge items. The group stages a window of
@@ -206,19 +212,20 @@ __host__ __device__ constexpr size_t merge_smem_bytes() {
 // accumulated, independent of row boundaries, so U loads stay in flight
 // across rows.
 template <int SUBW, int VEC, int EPI, bool ADD, int U, bool FULL, class Op>
-__global__ void __launch_bounds__(256, 3) merge_kernel(SegOut o, MergeShape ms, Op op) {
+__global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, Op op) {
   static_assert(U <= kStagePad, "ring deeper than the staging pad");
   using Item = typename Op::Item;
   constexpr int NG = 256 / SUBW;
   constexpr int SW = SUBW * VEC;
-  constexpr int CAP = merge_stage_cap<SUBW>();
+  constexpr int CAP = merge_stage_cap<SUBW, Op>();
+  constexpr int CAPR = merge_rows_cap<SUBW, Op>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* Hs = reinterpret_cast<float*>(smem_raw);                       // [NG][SW]
   float* Ts = Hs + NG * SW;                                             // [NG][SW]
   int* Hrow = reinterpret_cast<int*>(Ts + NG * SW);                     // [NG]
   int* Trow = Hrow + NG;                                                // [NG]
   Item* items_all = reinterpret_cast<Item*>(Trow + NG);                 // [NG][CAP]
-  int* rend_all = reinterpret_cast<int*>(items_all + NG * (CAP + kStagePad));  // [NG][CAP]
+  int* rend_all = reinterpret_cast<int*>(items_all + NG * (CAP + kStagePad));  // [NG][CAPR]
 
   const int sub = threadIdx.x / SUBW;
   const int lane = threadIdx.x % SUBW;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(256, 3) merge_kernel(SegOut o, MergeShape ms, 
   const int col0 = slab * SW + lane * VEC;
   const bool col_ok = FULL || col0 < o.k;
   Item* items = items_all + sub * (CAP + kStagePad);
-  int* rend = rend_all + sub * CAP;
+  int* rend = rend_all + sub * CAPR;
 
   if (z) {
     op.val += z * ms.batch_val_stride;
@@ -247,11 +254,11 @@ __global__ void __launch_bounds__(256, 3) merge_kernel(SegOut o, MergeShape ms, 
   const int n_rows = e.x - s.x;   // rows whose end item this group owns
   const int n_nnz = e.y - s.y;    // entries this group accumulates
 
-  // row ends of rows [row0 + rb, row0 + rb + CAP), relative to s.y
+  // row ends of rows [row0 + rb, row0 + rb + CAPR), relative to s.y
   int rb = 0;
   auto stage_rows = [&](int base) {
     __syncwarp(mask);
-    for (int t = lane; t < CAP && base + t < n_rows; t += SUBW)
+    for (int t = lane; t < CAPR && base + t < n_rows; t += SUBW)
       rend[t] = ld_stream(o.rowptr + row0 + base + 1 + t) - s.y;
     __syncwarp(mask);
   };
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(256, 3) merge_kernel(SegOut o, MergeShape ms, 
     acc.zero();
     ++r;
     cur_start = cur_end;
-    if (r - rb == CAP) {
+    if (r - rb == CAPR) {
       rb = r;
       stage_rows(rb);
     }

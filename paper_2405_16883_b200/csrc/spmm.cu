@@ -179,6 +179,71 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
 
 }  // namespace
 
+namespace {
+template <int SUBW, int VEC, class Op>
+int plan_ipg(int m, long long nnz, int k, int batch) {
+  constexpr int U = SUBW >= 8 ? Op::kRing : 4;
+  constexpr int NG = kThreads / SUBW;
+  constexpr int CAP = merge_stage_cap<SUBW, Op>();
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto kern = merge_kernel<SUBW, VEC, EPI_NONE, false, U, true, Op>;
+  const size_t smem = merge_smem_bytes<SUBW, VEC, Op>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const long long slabs = ceil_div(k, SUBW * VEC);
+  const long long total = (long long)m + nnz;
+  const long long cta_slots = (long long)sms * per_sm;
+  // CTAs available per (slab, batch) in one wave
+  long long ctas = cta_slots / (slabs * batch);
+  if (ctas < 1) ctas = 1;
+  long long waves = ceil_div(total, ctas * NG * (long long)CAP);
+  if (waves < 1) waves = 1;
+  long long ipg = ceil_div(total, ctas * waves * NG);
+  if (ipg < 32) ipg = 32;
+  if (ipg > kMaxIpg) ipg = kMaxIpg;
+  return (int)ipg;
+}
+}  // namespace
+
+extern "C" int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind) {
+  if (m < 0 || nnz < 0 || k < 1 || batch < 1) return fail(STC_EINVAL, "bad plan arguments");
+  const int vec = k % 4 == 0 ? 4 : 1;
+  const int subw = choose_subw(k, vec);
+  if (kind == 1) {
+    if (vec == 4) {
+      switch (subw) {
+        case 4: return plan_ipg<4, 4, MttkrpOp<4>>(m, nnz, k, batch);
+        case 8: return plan_ipg<8, 4, MttkrpOp<4>>(m, nnz, k, batch);
+        case 16: return plan_ipg<16, 4, MttkrpOp<4>>(m, nnz, k, batch);
+        default: return plan_ipg<32, 4, MttkrpOp<4>>(m, nnz, k, batch);
+      }
+    }
+    switch (subw) {
+      case 4: return plan_ipg<4, 1, MttkrpOp<1>>(m, nnz, k, batch);
+      case 8: return plan_ipg<8, 1, MttkrpOp<1>>(m, nnz, k, batch);
+      case 16: return plan_ipg<16, 1, MttkrpOp<1>>(m, nnz, k, batch);
+      default: return plan_ipg<32, 1, MttkrpOp<1>>(m, nnz, k, batch);
+    }
+  }
+  if (vec == 4) {
+    switch (subw) {
+      case 4: return plan_ipg<4, 4, SpmmOp<4>>(m, nnz, k, batch);
+      case 8: return plan_ipg<8, 4, SpmmOp<4>>(m, nnz, k, batch);
+      case 16: return plan_ipg<16, 4, SpmmOp<4>>(m, nnz, k, batch);
+      default: return plan_ipg<32, 4, SpmmOp<4>>(m, nnz, k, batch);
+    }
+  }
+  switch (subw) {
+    case 4: return plan_ipg<4, 1, SpmmOp<1>>(m, nnz, k, batch);
+    case 8: return plan_ipg<8, 1, SpmmOp<1>>(m, nnz, k, batch);
+    case 16: return plan_ipg<16, 1, SpmmOp<1>>(m, nnz, k, batch);
+    default: return plan_ipg<32, 1, SpmmOp<1>>(m, nnz, k, batch);
+  }
+}
+
 extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {
   if (items_per_group < 1 || m < 0 || nnz < 0) return -1;
   return n_groups_for(m, nnz, items_per_group);

@@ -175,9 +175,9 @@ def _stats(t: Tensor, view: RowView, key) -> ops.RowStats:
     return _cache(t, ("stats",) + key, lambda: ops.row_stats(view.rowptr))
 
 
-def _partition(t: Tensor, view: RowView, key, ipg: int) -> ops.MergePartition:
-    return _cache(t, ("partition", ipg) + key,
-                  lambda: ops.merge_partition(view.rowptr, view.vals.numel(), ipg))
+def _partition(t: Tensor, view: RowView, key, k: int) -> ops.MergePartition:
+    return _cache(t, ("partition", k) + key,
+                  lambda: ops.merge_partition(view.rowptr, view.vals.numel(), k=k))
 
 
 # ---------------------------------------------------------------------------
@@ -421,7 +421,7 @@ def _spmm_rows(ctx: _Ctx, m: _SpmmTerm, addend: torch.Tensor | None = None, relu
     variant = ctx.variant or ops.choose_variant(stats, K, aligned=(K % 4 == 0))
     if variant not in ("row", "merge", "coltile"):
         raise ValueError(f"unknown variant {variant!r}")
-    partition = _partition(A, view, key, ops.DEFAULT_ITEMS_PER_GROUP) if variant == "merge" else None
+    partition = _partition(A, view, key, K) if variant == "merge" else None
     if addend is not None and not view.dense_rows:
         raise UnsupportedExpressionError("dense addend with a compressed row level")
     Y = ops.spmm_csr(view.rowptr, view.cols, view.vals, Bd, addend=addend, relu=relu,
@@ -534,7 +534,7 @@ def _exec_batched_pv(ctx: _Ctx, pv: _BatchedPvTerm) -> torch.Tensor:
         stats = _cache(P, ("stats", "shared"), lambda: ops.row_stats(rowptr))
         variant = ctx.variant if ctx.variant in ("row", "merge") else (
             "merge" if stats.skew > ops.MERGE_SKEW_THRESHOLD else "row")
-        part = _cache(P, ("partition", "shared"), lambda: ops.merge_partition(rowptr, colidx.numel())) \
+        part = _cache(P, ("partition", "shared"), lambda: ops.merge_partition(rowptr, colidx.numel(), k=d, batch=H)) \
             if variant == "merge" else None
         O = ops.spmm_csr_batched(rowptr, colidx, vals, Vd, variant=variant, partition=part, stats=stats)
         ctx.chosen.append(f"pv:batched-{variant}")
@@ -552,7 +552,7 @@ def _exec_batched_pv(ctx: _Ctx, pv: _BatchedPvTerm) -> torch.Tensor:
         variant = ctx.variant if ctx.variant in ("row", "merge") else ops.choose_variant(stats, d)
         if variant == "coltile":
             variant = "merge"
-        part = _cache(P, ("partition", "flat"), lambda: ops.merge_partition(L.pos, nnz_total)) \
+        part = _cache(P, ("partition", "flat"), lambda: ops.merge_partition(L.pos, nnz_total, k=d)) \
             if variant == "merge" else None
         O = ops.spmm_csr(L.pos, cols, P.storage.values, Vd.reshape(H * n, d), variant=variant,
                          partition=part, stats=stats).reshape(H, m, d)
@@ -644,7 +644,8 @@ def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
     else:
         jc, kc = st.levels[1].crd, st.levels[2].crd
     variant = ctx.variant if ctx.variant in ("row", "merge") else "merge"
-    part = _cache(T, ("partition", "mttkrp"), lambda: ops.merge_partition(seg.ptr, st.values.numel())) \
+    part = _cache(T, ("partition", "mttkrp", Bd.shape[1]),
+                  lambda: ops.merge_partition(seg.ptr, st.values.numel(), k=Bd.shape[1], kind="mttkrp")) \
         if variant == "merge" else None
     M = ops.mttkrp_coo3(seg, jc, kc, st.values, Bd, Cd, variant=variant, partition=part)
     ctx.chosen.append(f"mttkrp:{variant}")

@@ -17,8 +17,9 @@ import torch
 from . import _abi
 from ._abi import check, lib, ptr, require_cuda, stream_handle
 
-# Items (row ends + stored entries) per sub-warp in the merge-path split.
-DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "256"))
+# Items (row ends + stored entries) per sub-warp in the merge-path split; 0 means
+# "plan it": whole waves of resident CTAs (stc_merge_plan_items_per_group).
+DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "0"))
 # Row-length skew (max / mean) above which the nnz-balanced split is chosen.
 MERGE_SKEW_THRESHOLD = 8.0
 # Dense widths above which the column-tiled variant is chosen.
@@ -98,11 +99,21 @@ class MergePartition:
     n_groups: int
 
 
-def merge_partition(rowptr: torch.Tensor, nnz: int,
-                    items_per_group: int = DEFAULT_ITEMS_PER_GROUP) -> MergePartition:
+def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "spmm") -> int:
+    ipg = int(lib().stc_merge_plan_items_per_group(m, nnz, max(k, 1), batch, 1 if kind == "mttkrp" else 0))
+    if ipg < 0:
+        check(ipg, "stc_merge_plan_items_per_group")
+    return ipg
+
+
+def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None = None, *,
+                    k: int = 128, batch: int = 1, kind: str = "spmm") -> MergePartition:
+    """Plan-time merge-path partition; ``items_per_group`` None/0 = planned for ``k``."""
     require_cuda(rowptr)
     _i32(rowptr)
     m = rowptr.numel() - 1
+    if not items_per_group:
+        items_per_group = DEFAULT_ITEMS_PER_GROUP or plan_items_per_group(m, nnz, k, batch, kind)
     groups = int(lib().stc_merge_path_groups(m, nnz, items_per_group))
     starts = torch.empty(2 * (groups + 1), dtype=torch.int32, device=rowptr.device)
     rc = lib().stc_merge_path_partition(m, nnz, ptr(rowptr), items_per_group, ptr(starts),
@@ -149,7 +160,7 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
     v = _abi.VARIANTS[variant]
     ipg = 0
     if variant == "merge":
-        partition = partition or merge_partition(rowptr, nnz)
+        partition = partition or merge_partition(rowptr, nnz, k=k)
         ipg = partition.items_per_group
         if workspace is None:
             workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
@@ -185,7 +196,7 @@ def spmm_csr_batched(rowptr, colidx, vals: torch.Tensor, B: torch.Tensor, *,
         variant = "row"
     ipg = 0
     if variant == "merge":
-        partition = partition or merge_partition(rowptr, nnz)
+        partition = partition or merge_partition(rowptr, nnz, k=k, batch=Z)
         ipg = partition.items_per_group
         if workspace is None:
             workspace = spmm_workspace(m, nnz, k, variant, ipg, Z, B.device)
@@ -327,7 +338,7 @@ def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tenso
     M = torch.empty((n_seg, R), dtype=torch.float32, device=B.device)
     ipg = 0
     if variant == "merge":
-        partition = partition or merge_partition(seg.ptr, nnz)
+        partition = partition or merge_partition(seg.ptr, nnz, k=R, kind="mttkrp")
         ipg = partition.items_per_group
         if workspace is None:
             workspace = spmm_workspace(n_seg, nnz, R, "merge", ipg, 1, B.device)

@@ -43,8 +43,9 @@ sys.argv = [a for a in sys.argv if not a.startswith("persist=")]
 if PERSIST:
     got = ops.l2_set_persisting(int(float(PERSIST[0].split("=")[1]) * 2**20))
     print("persisting L2 carve-out:", got / 2**20, "MiB")
-for ipg in [int(x) for x in (sys.argv[1:] or ["32", "64", "128", "256", "512"])]:
-    part = ops.merge_partition(R, A.nnz, ipg)
+for ipg in [int(x) for x in (sys.argv[1:] or ["0", "256", "512"])]:
+    part = ops.merge_partition(R, A.nnz, ipg, k=128)
+    ipg = part.items_per_group
     ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", ipg, 1, "cuda")
     ms = timeit(lambda: ops.spmm_csr(R, C, V, Z, out=out, variant="merge", partition=part, workspace=ws))
     print(f"merge ipg={ipg:4d}: {ms*1e3:8.1f} us  {byts/ms/1e6:8.1f} GB/s")
