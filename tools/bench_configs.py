@@ -1,0 +1,204 @@
+"""Per-configuration measurement on one B200 (all five BASELINE configs).
+
+For each config: GPU time of the hot-path kernel(s) with CUDA events (median
+over reps, L2 flushed before every rep), GFLOP/s, compulsory-byte GB/s and the
+roofline fraction (HBM for the bandwidth-bound configs, FP32 CUDA-core FMA for
+the compute-bound FFN / attention), plus the CPU oracle port timed on this
+host (C restatement, all threads) on a bounded sample, extrapolated by nnz.
+
+  python tools/bench_configs.py [--out profiles/configs_r01.json] [--configs 1,2,3,4,5]
+"""
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from oracle import native  # noqa: E402
+from paper_2405_16883_b200 import ops, synthetic  # noqa: E402
+
+torch.backends.cuda.matmul.allow_tf32 = False
+FLUSH = torch.empty(128 * 1024 * 1024, device="cuda")
+PROPS = torch.cuda.get_device_properties(0)
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())["hbm_gbs"], "measured"
+    return 6650.0, "fallback"
+
+
+def fp32_peak_tflops(mhz=1965.0):
+    return PROPS.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def gpu_time(fn, reps=20):
+    ts = []
+    fn()
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        FLUSH.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.median(ts)
+
+
+def cpu_time(fn, min_s=2.0):
+    fn()
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        fn()
+        n += 1
+        if time.perf_counter() - t0 > min_s:
+            break
+    return (time.perf_counter() - t0) / n
+
+
+def dev_csr(A):
+    return (torch.from_numpy(A.rowptr).int().cuda(), torch.from_numpy(A.colidx).int().cuda(),
+            torch.from_numpy(A.vals).cuda())
+
+
+def record(name, ms, flops, nbytes, bound, cpu_s, cpu_note, extra=None):
+    peak_gbs, kind = hbm_peak()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    gf = flops / (ms * 1e-3) / 1e9
+    r = {"config": name, "gpu_ms": round(ms, 5), "gflops": round(gf, 1), "compulsory_bytes": int(nbytes),
+         "gbs": round(gbs, 1), "frac_hbm_measured": round(gbs / peak_gbs, 4), "frac_hbm_8tbs": round(gbs / 8000, 4),
+         "hbm_peak_source": kind, "bound": bound,
+         "cpu_oracle_s": round(cpu_s, 4), "cpu_gflops": round(flops / cpu_s / 1e9, 3),
+         "cpu_threads": native.num_threads(), "cpu_note": cpu_note, "speedup_vs_cpu_oracle": round(cpu_s * 1e3 / ms, 1)}
+    if bound == "fp32":
+        r["frac_fp32_peak"] = round(gf / 1e3 / fp32_peak_tflops(), 4)
+        r["fp32_peak_tflops"] = round(fp32_peak_tflops(), 1)
+    if extra:
+        r.update(extra)
+    print(json.dumps(r), flush=True)
+    return r
+
+
+def cfg1():
+    A, B = synthetic.cfg1()
+    R, C, V = dev_csr(A)
+    Bt = torch.from_numpy(B).cuda()
+    out = torch.empty((A.shape[0], 64), device="cuda")
+    stats = ops.row_stats(R)
+    variant = ops.choose_variant(stats, 64)
+    ms = gpu_time(lambda: ops.spmm_csr(R, C, V, Bt, out=out, variant=variant, stats=stats))
+    flops = 2.0 * A.nnz * 64
+    nbytes = 4 * (A.shape[0] + 1) + 8 * A.nnz + 2 * 4 * 4096 * 64
+    v64, b64 = A.vals.astype(np.float64), B.astype(np.float64)
+    cs = cpu_time(lambda: native.spmm_csr(A.rowptr, A.colidx, v64, b64))
+    return record("cfg1_csr_spmm_4096_1pct_k64", ms, flops, nbytes, "hbm(L2-resident)", cs, "full",
+                  {"variant": variant, "nnz": A.nnz})
+
+
+def cfg2():
+    A, X, W1, W2 = synthetic.cfg2()
+    R, C, V = dev_csr(A)
+    Z = torch.from_numpy(X).cuda() @ torch.from_numpy(W1).cuda()
+    out = torch.empty_like(Z)
+    stats = ops.row_stats(R)
+    part = ops.merge_partition(R, A.nnz, k=128)
+    ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", part.items_per_group, 1, "cuda")
+    ms = gpu_time(lambda: ops.spmm_csr(R, C, V, Z, out=out, relu=True, variant="merge", partition=part,
+                                       workspace=ws, stats=stats))
+    flops = 2.0 * A.nnz * 128
+    nbytes = 4 * (A.shape[0] + 1) + 8 * A.nnz + 2 * 4 * A.shape[0] * 128
+    z64, v64 = Z.double().cpu().numpy(), A.vals.astype(np.float64)
+    cs = cpu_time(lambda: native.spmm_csr(A.rowptr, A.colidx, v64, z64, relu=True))
+    return record("cfg2_gcn_spmm_layer_relu", ms, flops, nbytes, "hbm", cs, "full layer",
+                  {"variant": "merge", "items_per_group": part.items_per_group, "nnz": A.nnz,
+                   "max_row": stats.max_row})
+
+
+def cfg3():
+    W, XT = synthetic.cfg3()
+    R, C, V = dev_csr(W)
+    Xt = torch.from_numpy(XT).cuda()
+    out = torch.empty((W.shape[0], 4096), device="cuda")
+    ms = gpu_time(lambda: ops.spmm_csr(R, C, V, Xt, out=out, variant="coltile"), reps=10)
+    flops = 2.0 * W.nnz * 4096
+    nbytes = 4 * (W.shape[0] + 1) + 8 * W.nnz + 4 * 4096 * 4096 + 4 * W.shape[0] * 4096
+    v64, x64 = W.vals.astype(np.float64), XT.astype(np.float64)
+    rows = 64
+    cs = cpu_time(lambda: native.spmm_csr(W.rowptr, W.colidx, v64, x64, rows=(0, rows)), 3.0)
+    cs *= W.shape[0] / rows
+    return record("cfg3_pruned_ffn_coltile", ms, flops, nbytes, "fp32", cs,
+                  f"rows [0,{rows}) extrapolated x{W.shape[0] // rows}", {"variant": "coltile", "nnz": W.nnz})
+
+
+def cfg4():
+    M, Q, K, V = synthetic.cfg4()
+    R, C, MV = dev_csr(M)
+    Qt, Kt, Vt = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+    ms = gpu_time(lambda: ops.sparse_attention(R, C, Qt, Kt, Vt, maskvals=MV, scale=0.125))
+
+    def unfused():
+        S = ops.sddmm_csr(R, C, Qt, Kt, maskvals=MV, scale=0.125)
+        ops.segment_softmax_(R, S)
+        return ops.spmm_csr_batched(R, C, S, Vt)
+
+    ms_unfused = gpu_time(unfused)
+    H = 16
+    flops = 4.0 * 64 * H * M.nnz
+    nbytes = 4 * (M.shape[0] + 1) + 8 * M.nnz + 4 * 4 * H * 8192 * 64
+    q64, k64, v64 = Q[0].astype(np.float64), K[0].astype(np.float64), V[0].astype(np.float64)
+
+    def one_head():
+        s = 0.125 * native.sddmm_csr(M.rowptr, M.colidx, None, q64, k64)
+        p = native.segment_softmax(M.rowptr, s)
+        native.spmm_csr(M.rowptr, M.colidx, p, v64)
+
+    cs = cpu_time(one_head) * H
+    return record("cfg4_sparse_attention_fused", ms, flops, nbytes, "fp32", cs, "1 head x16",
+                  {"unfused_ms": round(ms_unfused, 4), "nnz_per_head": M.nnz})
+
+
+def cfg5():
+    (i, j, k), vals, B, C = synthetic.cfg5()
+    It, Jt, Kt = (torch.from_numpy(x).int().cuda() for x in (i, j, k))
+    Vt = torch.from_numpy(vals).cuda()
+    seg = ops.coo_segments(It)
+    Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
+    part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp")
+    ms = gpu_time(lambda: ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part))
+    nnz = len(vals)
+    flops = 3.0 * nnz * 32
+    nbytes = 16 * nnz + 2 * 4 * 20000 * 32 + 4 * seg.n_seg * 32
+    first = np.ones(nnz, bool)
+    first[1:] = i[1:] != i[:-1]
+    ptr = np.append(np.flatnonzero(first), nnz)
+    v64, b64, c64 = vals.astype(np.float64), B.astype(np.float64), C.astype(np.float64)
+    cs = cpu_time(lambda: native.mttkrp(ptr, j, k, v64, b64, c64))
+    return record("cfg5_mttkrp_zipf_coo3", ms, flops, nbytes, "hbm", cs, "full",
+                  {"nnz": nnz, "items_per_group": part.items_per_group, "row0_nnz": int(ptr[1])})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    a = ap.parse_args()
+    fns = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
+    res = [fns[int(c)]() for c in a.configs.split(",")]
+    if a.out:
+        Path(a.out).write_text(json.dumps({"device": PROPS.name, "sms": PROPS.multi_processor_count,
+                                           "results": res}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
