@@ -80,6 +80,12 @@ int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_
  * partial last wave idles SMs. `kind` 0 = SpMM, 1 = MTTKRP.                  */
 int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind);
 
+/* Plan of the COLTILE variant: per row, the first entry of every 128-column
+ * chunk of A (int32, stc_coltile_plan_ints(m, n) values). Pass it as the
+ * `partition` argument of a COLTILE SpMM.                                    */
+long long stc_coltile_plan_ints(int m, int n);
+int stc_coltile_plan(int m, int n, const int* rowptr, const int* colidx, int* chunk_ptr, void* stream);
+
 /* Workspace for the MERGE variant (carry buffers); 0 for ROW/COLTILE.        */
 size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int items_per_group,
                                 int batch);
@@ -88,7 +94,8 @@ size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int it
  * Replaces the dense-output driver + vectorised tail of the reference,
  * engine.py:487-573 (`_run_dense_output`, `vector_sink`), for
  * C(i,k) = A(i,j) * B(j,k) [+ D(i,k)] with A CSR, B/D dense.
- * n = columns of A (rows of B); D nullable; partition required for MERGE.   */
+ * n = columns of A (rows of B); D nullable; `partition` = the merge-path
+ * starts for MERGE, the chunk plan for COLTILE, ignored for ROW.            */
 int stc_spmm_csr_f32(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
                      long long nnz, const float* B, long long ldb, float* C, long long ldc,
                      const float* D, long long ldd, int variant, int epilogue, const int* partition,

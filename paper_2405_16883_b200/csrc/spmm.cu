@@ -101,18 +101,18 @@ int dispatch_spmm(int epilogue, bool add, const SegOut& o, const MergeShape& ms,
 }
 
 template <int EPI, bool ADD>
-int launch_coltile(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
+int launch_coltile(int m, int n, int k, const int* chunk_ptr, const int* colidx, const float* vals,
                    const float* B, long long ldb, float* C, long long ldc, const float* D, long long ldd,
-                   cudaStream_t st) {
-  const size_t smem = 2 * CT_CHUNK * CT_COLS * sizeof(float);
+                   cudaStream_t st, const Launch& L) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(coltile_kernel<EPI, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(coltile_kernel<EPI, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM);
     configured = true;
   }
   if (m == 0 || k == 0) return STC_OK;
   const dim3 grid((unsigned)ceil_div(m, CT_ROWS), (unsigned)ceil_div(k, CT_COLS));
-  coltile_kernel<EPI, ADD><<<grid, 256, smem, st>>>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd);
+  launch_windowed(coltile_kernel<EPI, ADD>, grid, dim3(CT_THREADS), CT_SMEM, st, L.window, L.window_bytes, m, n,
+                  k, chunk_ptr, colidx, vals, B, ldb, C, ldc, D, ldd);
   return check_launch("coltile_kernel");
 }
 
@@ -138,11 +138,14 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
   if (variant == STC_VARIANT_COLTILE) {
     if (!vec4) return fail(STC_EUNSUPPORTED, "COLTILE needs k, ldb, ldc multiples of 4 and 16-byte alignment");
     if (batch != 1) return fail(STC_EUNSUPPORTED, "COLTILE is not batched");
+    if (!partition) return fail(STC_EINVAL, "COLTILE needs its plan (stc_coltile_plan) as `partition`");
+    const Launch L{variant, 1, st, B, (size_t)((long long)n * ldb) * sizeof(float)};
+    const int* cp = partition;
     if (epilogue == STC_EPILOGUE_RELU)
-      return D ? launch_coltile<EPI_RELU, true>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st)
-               : launch_coltile<EPI_RELU, false>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st);
-    return D ? launch_coltile<EPI_NONE, true>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st)
-             : launch_coltile<EPI_NONE, false>(m, n, k, rowptr, colidx, vals, B, ldb, C, ldc, D, ldd, st);
+      return D ? launch_coltile<EPI_RELU, true>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L)
+               : launch_coltile<EPI_RELU, false>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L);
+    return D ? launch_coltile<EPI_NONE, true>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L)
+             : launch_coltile<EPI_NONE, false>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L);
   }
   if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
     return fail(STC_EINVAL, "unknown variant %d", variant);
@@ -242,6 +245,21 @@ extern "C" int stc_merge_plan_items_per_group(int m, long long nnz, int k, int b
     case 16: return plan_ipg<16, 1, SpmmOp<1>>(m, nnz, k, batch);
     default: return plan_ipg<32, 1, SpmmOp<1>>(m, nnz, k, batch);
   }
+}
+
+extern "C" long long stc_coltile_plan_ints(int m, int n) {
+  if (m < 0 || n < 0) return -1;
+  return (long long)m * (ceil_div(n, CT_CHUNK) + 1);
+}
+
+extern "C" int stc_coltile_plan(int m, int n, const int* rowptr, const int* colidx, int* chunk_ptr, void* stream) {
+  if (m < 0 || n < 0) return fail(STC_EINVAL, "negative extent");
+  if (m == 0) return STC_OK;
+  if (!rowptr || !chunk_ptr) return fail(STC_EINVAL, "null pointer");
+  const int n_chunks = (int)ceil_div(n, CT_CHUNK);
+  coltile_plan_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      m, n_chunks, rowptr, colidx, chunk_ptr);
+  return check_launch("coltile_plan_kernel");
 }
 
 extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {

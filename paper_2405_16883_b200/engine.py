@@ -421,7 +421,11 @@ def _spmm_rows(ctx: _Ctx, m: _SpmmTerm, addend: torch.Tensor | None = None, relu
     variant = ctx.variant or ops.choose_variant(stats, K, aligned=(K % 4 == 0))
     if variant not in ("row", "merge", "coltile"):
         raise ValueError(f"unknown variant {variant!r}")
-    partition = _partition(A, view, key, K) if variant == "merge" else None
+    partition = None
+    if variant == "merge":
+        partition = _partition(A, view, key, K)
+    elif variant == "coltile":
+        partition = _cache(A, ("coltile",) + key, lambda: ops.coltile_plan(view.rowptr, view.cols, Bd.shape[0]))
     if addend is not None and not view.dense_rows:
         raise UnsupportedExpressionError("dense addend with a compressed row level")
     Y = ops.spmm_csr(view.rowptr, view.cols, view.vals, Bd, addend=addend, relu=relu,

@@ -122,6 +122,23 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
     return MergePartition(starts, items_per_group, groups)
 
 
+@dataclass
+class ColtilePlan:
+    """Per-row chunk starts for the COLTILE variant (int32 [m, n_chunks + 1])."""
+
+    chunk_ptr: torch.Tensor
+
+
+def coltile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, n_cols: int) -> ColtilePlan:
+    require_cuda(rowptr, colidx)
+    m = rowptr.numel() - 1
+    ints = int(lib().stc_coltile_plan_ints(m, n_cols))
+    cp = torch.empty(max(ints, 1), dtype=torch.int32, device=rowptr.device)
+    check(lib().stc_coltile_plan(m, n_cols, ptr(rowptr), ptr(colidx), ptr(cp), stream_handle()),
+          "stc_coltile_plan")
+    return ColtilePlan(cp)
+
+
 def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int, batch: int,
                    device) -> torch.Tensor | None:
     n = int(lib().stc_spmm_workspace_bytes(m, nnz, k, _abi.VARIANTS[variant], items_per_group, batch))
@@ -138,9 +155,13 @@ def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int,
 def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor,
              *, out: torch.Tensor | None = None, addend: torch.Tensor | None = None,
              relu: bool = False, variant: str | None = None,
-             partition: MergePartition | None = None, workspace: torch.Tensor | None = None,
+             partition=None, workspace: torch.Tensor | None = None,
              stats: RowStats | None = None) -> torch.Tensor:
-    """``C = act(A @ B + addend)`` with A in CSR (int32 rowptr/colidx, fp32 vals)."""
+    """``C = act(A @ B + addend)`` with A in CSR (int32 rowptr/colidx, fp32 vals).
+
+    ``partition``: a ``MergePartition`` for "merge", a ``ColtilePlan`` for "coltile"
+    (computed here when omitted; cache it with the matrix for repeated calls).
+    """
     require_cuda(rowptr, colidx, vals, B)
     _i32(rowptr), _i32(colidx), _f32(vals), _f32(B)
     if B.dim() != 2 or B.stride(1) != 1:
@@ -159,17 +180,21 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
         variant = choose_variant(stats, k, aligned=(k % 4 == 0))
     v = _abi.VARIANTS[variant]
     ipg = 0
+    plan_ptr = None
     if variant == "merge":
         partition = partition or merge_partition(rowptr, nnz, k=k)
         ipg = partition.items_per_group
+        plan_ptr = ptr(partition.starts)
         if workspace is None:
             workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
+    elif variant == "coltile":
+        partition = partition or coltile_plan(rowptr, colidx, n)
+        plan_ptr = ptr(partition.chunk_ptr)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_spmm_csr_f32(
         m, n, k, ptr(rowptr), ptr(colidx), ptr(vals), nnz, ptr(B), B.stride(0), ptr(out),
         out.stride(0), ptr(addend), 0 if addend is None else addend.stride(0), v,
-        _abi.EPILOGUE_RELU if relu else _abi.EPILOGUE_NONE,
-        None if partition is None else ptr(partition.starts), ipg, ptr(workspace), ws_bytes,
+        _abi.EPILOGUE_RELU if relu else _abi.EPILOGUE_NONE, plan_ptr, ipg, ptr(workspace), ws_bytes,
         stream_handle())
     check(rc, "stc_spmm_csr_f32")
     return out
