@@ -457,7 +457,7 @@ def run_ours(args):
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "SpMM layer = merge_kernel + merge_fixup_kernel (events around both)",
+            "kernel": "SpMM layer = one merge_kernel launch (carries fixed up in-kernel by the last arriving CTA)",
             "algorithmic_bytes_per_launch": work.bytes_per_step,
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
             else "fallback 6.65 TB/s (B200_PROFILING.md)",

@@ -86,7 +86,9 @@ int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int k
 long long stc_coltile_plan_ints(int m, int n);
 int stc_coltile_plan(int m, int n, const int* rowptr, const int* colidx, int* chunk_ptr, void* stream);
 
-/* Workspace for the MERGE variant (carry buffers); 0 for ROW/COLTILE.        */
+/* Workspace for the MERGE variant (carry buffers + per-CTA arrival counters);
+ * 0 for ROW/COLTILE. It must be ZERO-FILLED once when allocated; every launch
+ * leaves the counters at zero again.                                        */
 size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int items_per_group,
                                 int batch);
 

@@ -17,9 +17,11 @@
 // owns; rows cut by group boundaries leave partial sums ("carries"):
 //   * inside a CTA the carries are combined through shared memory;
 //   * across CTAs each CTA leaves at most one tail carry and one head partial
-//     in a global workspace and a fix-up kernel combines them in position
-//     order and applies the epilogue.
-// No atomics anywhere, so results are bit-reproducible run to run, and the
+//     in a global workspace; the last CTA to publish a carry for a row (an
+//     arrival counter per row) combines them in position order and applies the
+//     epilogue — no second launch.
+// No atomic accumulation: the only atomics are arrival counters, every sum runs
+// in a fixed order, so results are bit-reproducible run to run, and the
 // epilogue (ReLU) is applied exactly once per row after its full reduction.
 #pragma once
 
@@ -44,7 +46,8 @@ struct SpmmOp {
   long long ldb;
   unsigned lane_off = 0;  // this lane's first column (added in 32-bit)
 
-  static constexpr int kRing = 8;  // gathers in flight per group
+  static constexpr int kRing = 8;           // gathers in flight per group
+  static constexpr int kStageBytes = 32768;  // staged items per CTA (rest of SMEM stays L1)
   struct Item {
     unsigned off;
     float v;
@@ -82,6 +85,7 @@ struct MttkrpOp {
   unsigned lane_off = 0;
 
   static constexpr int kRing = VEC == 4 ? 4 : 8;
+  static constexpr int kStageBytes = 16384;  // small: the hot factor rows live in L1
   struct __align__(16) Item {
     unsigned offb, offc;
     float v;
@@ -172,8 +176,9 @@ struct MergeShape {
   int n_groups;
   int ipg;               // items per group
   int n_cta;
-  float* head_buf;       // [slabs][n_cta][slab_w]
-  float* tail_buf;       // [slabs][n_cta][slab_w]
+  float* head_buf;       // [batch][slabs][n_cta][slab_w]
+  float* tail_buf;       // [batch][slabs][n_cta][slab_w]
+  int* counters;         // [batch][slabs][n_cta] arrival counters, zero between launches
   long long batch_val_stride;   // batched (multi-head) variants: per-z offsets
   long long batch_b_stride;
   long long batch_c_stride;
@@ -183,7 +188,7 @@ struct MergeShape {
 // per group), plus CAP/4 row ends per group (restaged when a group owns more rows).
 template <int SUBW, class Op>
 __host__ __device__ constexpr int merge_stage_cap() {
-  return 32768 / ((256 / SUBW) * (int)sizeof(typename Op::Item));
+  return Op::kStageBytes / ((256 / SUBW) * (int)sizeof(typename Op::Item));
 }
 template <int SUBW, class Op>
 __host__ __device__ constexpr int merge_rows_cap() {
@@ -337,98 +342,118 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
   __syncthreads();
 
   // ---- CTA-level combine (position order: tails of earlier groups, then head) ----
+  __shared__ int head_row_s, tail_row_s;
+  if (threadIdx.x == 0) head_row_s = tail_row_s = -1;
   const int2 cs = ms.starts[min(cta * NG, ms.n_groups)];
   const bool cta_head_mid = (cs.x < o.m) && (cs.y > o.rowptr[cs.x]);
+  __syncthreads();
   const int hr = Hrow[sub];
-  if (hr >= 0 && col_ok) {
+  if (hr >= 0) {
     int lo = sub;
     while (lo > 0 && Trow[lo - 1] == hr) --lo;
-    Frag<VEC> sum;
-    sum.zero();
-    for (int t = lo; t < sub; ++t) {
-      Frag<VEC> part;
-      part.load_plain(&Ts[t * SW + lane * VEC]);
+    const bool to_head = lo == 0 && cta_head_mid && hr == cs.x;  // began in an earlier CTA
+    if (col_ok) {
+      Frag<VEC> sum;
+      sum.zero();
+      for (int t = lo; t < sub; ++t) {
+        Frag<VEC> part;
+        part.load_plain(&Ts[t * SW + lane * VEC]);
 #pragma unroll
-      for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
-    }
-    Frag<VEC> h;
-    h.load_plain(&Hs[sub * SW + lane * VEC]);
+        for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
+      }
+      Frag<VEC> h;
+      h.load_plain(&Hs[sub * SW + lane * VEC]);
 #pragma unroll
-    for (int x = 0; x < VEC; ++x) sum.v[x] += h.v[x];
-    if (lo == 0 && cta_head_mid && hr == cs.x) {
-      sum.store_plain(ms.head_buf + (zslab + cta) * SW + lane * VEC);  // needs earlier CTAs
-    } else {
-      write_row<VEC, EPI, ADD>(o, hr, col0, sum);
+      for (int x = 0; x < VEC; ++x) sum.v[x] += h.v[x];
+      if (to_head) {
+        sum.store_plain(ms.head_buf + (zslab + cta) * SW + lane * VEC);
+      } else {
+        write_row<VEC, EPI, ADD>(o, hr, col0, sum);
+      }
     }
+    if (to_head && lane == 0) head_row_s = hr;
   }
-  if (sub == NG - 1 && Trow[sub] >= 0 && col_ok) {
+  if (sub == NG - 1 && Trow[sub] >= 0) {
     const int tr = Trow[sub];
     int lo = sub;
     while (lo > 0 && Trow[lo - 1] == tr && Hrow[lo] < 0) --lo;
+    if (col_ok) {
+      Frag<VEC> sum;
+      sum.zero();
+      for (int t = lo; t <= sub; ++t) {
+        Frag<VEC> part;
+        part.load_plain(&Ts[t * SW + lane * VEC]);
+#pragma unroll
+        for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
+      }
+      sum.store_plain(ms.tail_buf + (zslab + cta) * SW + lane * VEC);
+    }
+    if (lane == 0) tail_row_s = tr;
+  }
+
+  // ---- rows cut by CTA boundaries: the last CTA to publish its carry for a row
+  // sums every carry of that row in position order and writes it (no extra launch).
+  // Carries are published with a gpu-scope fence before the arrival counter.
+  __threadfence();
+  __syncthreads();
+  __shared__ int fix_row[2], fix_first[2], fix_last[2], n_fix;
+  if (threadIdx.x == 0) {
+    n_fix = 0;
+    const long long ci = (long long)NG * ms.ipg;
+    auto arrive = [&](int r, int c_last) {
+      const int c_first = (int)(((long long)o.rowptr[r] + r) / ci);
+      const int need = c_last - c_first + 1;
+      int* ctr = ms.counters + zslab + c_last;
+      if (atomicAdd(ctr, 1) + 1 == need) {
+        *ctr = 0;  // every participant has arrived: reset for the next launch
+        fix_row[n_fix] = r;
+        fix_first[n_fix] = c_first;
+        fix_last[n_fix] = c_last;
+        ++n_fix;
+      }
+    };
+    if (head_row_s >= 0) arrive(head_row_s, cta);
+    if (tail_row_s >= 0) {
+      const int r = tail_row_s;
+      arrive(r, (int)(((long long)o.rowptr[r + 1] + r) / ci));
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  for (int f = 0; f < n_fix; ++f) {
+    const int r = fix_row[f], c_first = fix_first[f], c_last = fix_last[f];
+    // sub-warp s sums tails c_first+s, c_first+s+NG, ... (ascending); sub-warp 0 then
+    // adds the NG partials in order and the head: fixed order, spread over the CTA.
     Frag<VEC> sum;
     sum.zero();
-    for (int t = lo; t <= sub; ++t) {
-      Frag<VEC> part;
-      part.load_plain(&Ts[t * SW + lane * VEC]);
+    if (col_ok) {
+      for (int t = c_first + sub; t < c_last; t += NG) {
+        Frag<VEC> p;
+        p.load_l2(ms.tail_buf + (zslab + t) * SW + lane * VEC);
 #pragma unroll
-      for (int x = 0; x < VEC; ++x) sum.v[x] += part.v[x];
+        for (int x = 0; x < VEC; ++x) sum.v[x] += p.v[x];
+      }
+      sum.store_plain(&Ts[sub * SW + lane * VEC]);
     }
-    sum.store_plain(ms.tail_buf + (zslab + cta) * SW + lane * VEC);
-  }
-}
-
-// Fix-up of rows cut by CTA boundaries: one sub-warp per boundary c >= 1 whose
-// CTA finishes a row that began in an earlier CTA. Sums, in position order,
-// the tail carries of CTAs c_first..c-1 and CTA c's head partial.
-template <int SUBW, int VEC, int EPI, bool ADD>
-__global__ void __launch_bounds__(256) merge_fixup_kernel(SegOut o, MergeShape ms) {
-  constexpr int NG = 256 / SUBW;
-  constexpr int SW = SUBW * VEC;
-  const int lane = threadIdx.x % SUBW;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) / SUBW + 1;
-  const int slab = blockIdx.y;
-  const int z = blockIdx.z;
-  if (c >= ms.n_cta) return;
-  const int col0 = slab * SW + lane * VEC;
-  if (col0 >= o.k) return;
-  if (z) {
-    o.C += z * ms.batch_c_stride;
-    if constexpr (ADD) o.D += z * ms.batch_c_stride;
-  }
-  const long long zslab = ((long long)z * gridDim.y + slab) * ms.n_cta;
-
-  const int2 cs = ms.starts[min(c * NG, ms.n_groups)];
-  const int r = cs.x;
-  if (r >= o.m) return;
-  const int rstart = o.rowptr[r];
-  if (cs.y <= rstart) return;  // boundary not inside row r
-  if (c + 1 < ms.n_cta && ms.starts[min((c + 1) * NG, ms.n_groups)].x == r) return;  // not finished here
-  const long long ci = (long long)NG * ms.ipg;
-  const int c_first = (int)(((long long)rstart + r) / ci);
-
-  Frag<VEC> sum;
-  sum.zero();
-  int t = c_first;
-  for (; t + 4 <= c; t += 4) {
-    Frag<VEC> p0, p1, p2, p3;
-    p0.load_plain(ms.tail_buf + (zslab + t) * SW + lane * VEC);
-    p1.load_plain(ms.tail_buf + (zslab + t + 1) * SW + lane * VEC);
-    p2.load_plain(ms.tail_buf + (zslab + t + 2) * SW + lane * VEC);
-    p3.load_plain(ms.tail_buf + (zslab + t + 3) * SW + lane * VEC);
+    __syncthreads();
+    if (sub == 0 && col_ok) {
+      Frag<VEC> tot;
+      tot.zero();
+      const int used = min(NG, c_last - c_first);
+      for (int s2 = 0; s2 < used; ++s2) {
+        Frag<VEC> p;
+        p.load_plain(&Ts[s2 * SW + lane * VEC]);
 #pragma unroll
-    for (int x = 0; x < VEC; ++x) sum.v[x] = (((sum.v[x] + p0.v[x]) + p1.v[x]) + p2.v[x]) + p3.v[x];
-  }
-  for (; t < c; ++t) {
-    Frag<VEC> p;
-    p.load_plain(ms.tail_buf + (zslab + t) * SW + lane * VEC);
+        for (int x = 0; x < VEC; ++x) tot.v[x] += p.v[x];
+      }
+      Frag<VEC> h;
+      h.load_l2(ms.head_buf + (zslab + c_last) * SW + lane * VEC);
 #pragma unroll
-    for (int x = 0; x < VEC; ++x) sum.v[x] += p.v[x];
+      for (int x = 0; x < VEC; ++x) tot.v[x] += h.v[x];
+      write_row<VEC, EPI, ADD>(o, r, col0, tot);
+    }
+    __syncthreads();
   }
-  Frag<VEC> h;
-  h.load_plain(ms.head_buf + (zslab + c) * SW + lane * VEC);
-#pragma unroll
-  for (int x = 0; x < VEC; ++x) sum.v[x] += h.v[x];
-  write_row<VEC, EPI, ADD>(o, r, col0, sum);
 }
 
 // ---------------------------------------------------------------------------

@@ -30,7 +30,8 @@ size_t merge_ws_bytes(int m, long long nnz, int k, int subw, int vec, int ipg, i
   const long long n_cta = ceil_div(groups, ng);
   const int sw = subw * vec;
   const long long slabs = ceil_div(k, sw);
-  return (size_t)(2LL * batch * slabs * n_cta * sw * (long long)sizeof(float));
+  return (size_t)(2LL * batch * slabs * n_cta * sw * (long long)sizeof(float) +
+                  batch * slabs * n_cta * (long long)sizeof(int));
 }
 
 struct Launch {
@@ -72,11 +73,7 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
   else
     launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>, grid, dim3(kThreads), smem, L.stream,
                     L.window, L.window_bytes, o, ms, op);
-  int rc = check_launch("merge_kernel");
-  if (rc || ms.n_cta < 2) return rc;
-  const dim3 fgrid((unsigned)ceil_div((long long)(ms.n_cta - 1) * SUBW, kThreads), slabs, L.batch);
-  merge_fixup_kernel<SUBW, VEC, EPI, ADD><<<fgrid, kThreads, 0, L.stream>>>(o, ms);
-  return check_launch("merge_fixup_kernel");
+  return check_launch("merge_kernel");
 }
 
 template <int VEC, int EPI, bool ADD, template <int> class OpT>
@@ -170,6 +167,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
     ms.ipg = ipg;
     ms.head_buf = static_cast<float*>(ws);
     ms.tail_buf = ms.head_buf + (long long)batch * slabs * n_cta * sw;
+    ms.counters = reinterpret_cast<int*>(ms.tail_buf + (long long)batch * slabs * n_cta * sw);
   }
   Launch L{variant, batch, st, B, (size_t)((long long)n * ldb * (batch > 1 && b_bs ? batch : 1)) * sizeof(float)};
   if (vec4) {
@@ -202,7 +200,8 @@ int plan_ipg(int m, long long nnz, int k, int batch) {
   // CTAs available per (slab, batch) in one wave
   long long ctas = cta_slots / (slabs * batch);
   if (ctas < 1) ctas = 1;
-  long long waves = ceil_div(total, ctas * NG * (long long)CAP);
+  const long long max_ipg = 8LL * CAP < kMaxIpg ? 8LL * CAP : kMaxIpg;  // a few staging windows per group
+  long long waves = ceil_div(total, ctas * NG * max_ipg);
   if (waves < 1) waves = 1;
   long long ipg = ceil_div(total, ctas * waves * NG);
   if (ipg < 32) ipg = 32;
@@ -400,6 +399,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
     ms.ipg = items_per_group;
     ms.head_buf = static_cast<float*>(ws);
     ms.tail_buf = ms.head_buf + ceil_div(rank, sw) * n_cta * sw;
+    ms.counters = reinterpret_cast<int*>(ms.tail_buf + ceil_div(rank, sw) * n_cta * sw);
   }
   Launch L{variant, 1, st, B, (size_t)((long long)n_j * ldb) * sizeof(float)};
   if (vec4) {

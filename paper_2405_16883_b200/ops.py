@@ -144,7 +144,8 @@ def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int,
     n = int(lib().stc_spmm_workspace_bytes(m, nnz, k, _abi.VARIANTS[variant], items_per_group, batch))
     if n == 0:
         return None
-    return torch.empty((n + 3) // 4, dtype=torch.float32, device=device)
+    # zero once: the arrival counters at its tail must start (and end) at zero
+    return torch.zeros((n + 3) // 4, dtype=torch.float32, device=device)
 
 
 # ---------------------------------------------------------------------------
