@@ -156,6 +156,21 @@ int stc_sparse_attention_f32(int m, int n, int d, int heads, const int* rowptr, 
                              const float* V, long long v_hs, long long v_rs, float scale, float* O,
                              long long o_hs, long long o_rs, float* S, float* P, void* stream);
 
+/* Block-tiled fused attention (head dim 64) for masks with dense bands: the
+ * plan (built by paper_2405_16883_b200.ops.attention_tile_plan) lists for every
+ * 64-row block up to dt_max dense 64-column tiles (tile_cols, -1 padded) with
+ * their mask values (tile_vals, NaN = absent) and a CSR remainder of all other
+ * entries. Dense tiles run as register-tiled QK^T / PV on CUDA cores with an
+ * online softmax; the remainder continues the same softmax per row.
+ * Workspace: stc_attention_tiled_workspace_bytes(m, heads).                 */
+size_t stc_attention_tiled_workspace_bytes(int m, int heads);
+int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, int n_blocks, int dt_max, const int* tile_cols,
+                                   const float* tile_vals, const int* rem_rowptr, const int* rem_colidx,
+                                   const float* rem_vals, long long rem_nnz, const float* Q, long long q_hs,
+                                   long long q_rs, const float* K, long long k_hs, long long k_rs, const float* V,
+                                   long long v_hs, long long v_rs, float scale, float* O, long long o_hs,
+                                   long long o_rs, void* ws, size_t ws_bytes, void* stream);
+
 /* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
  * M[s,:] = sum_{p in seg s} (vals[p] * B[j[p],:]) * C[k[p],:]
  * B has n_j rows, C has n_k rows (each below 2^32 elements: 32-bit gather offsets).

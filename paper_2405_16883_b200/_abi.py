@@ -65,6 +65,9 @@ SIGNATURES = {
     "stc_segsoftmax_csr_f32": (_i, [_i, _i, _p, _ll, _p, _p]),
     "stc_sparse_attention_f32": (_i, [_i, _i, _i, _i, _p, _p, _p, _ll, _p, _ll, _ll, _p, _ll, _ll, _p,
                                       _ll, _ll, _f, _p, _ll, _ll, _p, _p, _p]),
+    "stc_attention_tiled_workspace_bytes": (_sz, [_i, _i]),
+    "stc_sparse_attention_tiled_f32": (_i, [_i, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _ll, _p, _ll, _ll, _p, _ll,
+                                            _ll, _p, _ll, _ll, _f, _p, _ll, _ll, _p, _sz, _p]),
     "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _i, _p, _i,
                                  _p, _sz, _p]),
 }

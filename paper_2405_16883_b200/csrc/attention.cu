@@ -1,6 +1,7 @@
 // C-ABI entry points for SDDMM, segmented softmax and fused sparse attention.
 #include "abi_util.cuh"
 #include "attention.cuh"
+#include "attention_tiled.cuh"
 
 using namespace stc;
 
@@ -110,4 +111,60 @@ extern "C" int stc_sparse_attention_f32(int m, int n, int d, int heads, const in
   a.O = O; a.o_hs = o_hs; a.o_rs = o_rs;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return S ? attn_by_d<true>(a, st) : attn_by_d<false>(a, st);
+}
+
+extern "C" size_t stc_attention_tiled_workspace_bytes(int m, int heads) {
+  if (m <= 0 || heads <= 0) return 0;
+  return (size_t)heads * m * (AT_D * sizeof(float) + sizeof(float2));
+}
+
+extern "C" int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, int n_blocks, int dt_max,
+                                              const int* tile_cols, const float* tile_vals, const int* rem_rowptr,
+                                              const int* rem_colidx, const float* rem_vals, long long rem_nnz,
+                                              const float* Q, long long q_hs, long long q_rs, const float* K,
+                                              long long k_hs, long long k_rs, const float* V, long long v_hs,
+                                              long long v_rs, float scale, float* O, long long o_hs, long long o_rs,
+                                              void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_common(m, n, d, heads, rem_rowptr, rem_nnz);
+  if (rc) return rc;
+  if (m == 0) return STC_OK;
+  if (d != AT_D) return fail(STC_EUNSUPPORTED, "tiled attention needs head dim 64 (got %d)", d);
+  if (n_blocks != (int)ceil_div(m, AT_B) || dt_max < 0) return fail(STC_EINVAL, "bad tile plan shape");
+  if (!O || !Q || !K || !V || (dt_max && (!tile_cols || !tile_vals)) || (rem_nnz && (!rem_colidx || !rem_vals)))
+    return fail(STC_EINVAL, "null pointer");
+  const bool ok = aligned16(Q) && aligned16(K) && aligned16(V) && aligned16(O) && q_rs % 4 == 0 &&
+                  k_rs % 4 == 0 && v_rs % 4 == 0 && o_rs % 4 == 0 && q_hs % 4 == 0 && k_hs % 4 == 0 &&
+                  v_hs % 4 == 0 && o_hs % 4 == 0 && q_rs >= d && k_rs >= d && v_rs >= d && o_rs >= d;
+  if (!ok) return fail(STC_EINVAL, "Q/K/V/O must be 16-byte aligned with strides multiple of 4 and >= d");
+  const size_t need = stc_attention_tiled_workspace_bytes(m, heads);
+  if (!ws || ws_bytes < need || !aligned16(ws)) return fail(STC_EWORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TileArgs t{};
+  t.m = m; t.n = n; t.heads = heads; t.n_blocks = n_blocks; t.dt_max = dt_max;
+  t.tile_cols = tile_cols; t.tile_vals = tile_vals;
+  t.Q = Q; t.q_hs = q_hs; t.q_rs = q_rs;
+  t.K = K; t.k_hs = k_hs; t.k_rs = k_rs;
+  t.V = V; t.v_hs = v_hs; t.v_rs = v_rs;
+  t.scale = scale;
+  t.Opart = static_cast<float*>(ws);
+  t.ml = reinterpret_cast<float2*>(t.Opart + (size_t)heads * m * AT_D);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT_SMEM);
+    configured = true;
+  }
+  attn_tile_kernel<<<dim3(n_blocks, heads), AT_THREADS, AT_SMEM, st>>>(t);
+  rc = check_launch("attn_tile_kernel");
+  if (rc) return rc;
+  AttnArgs a{};
+  a.m = m; a.n = n; a.d = d; a.heads = heads;
+  a.rowptr = rem_rowptr; a.colidx = rem_colidx; a.maskv = rem_vals;
+  a.Q = Q; a.q_hs = q_hs; a.q_rs = q_rs;
+  a.K = K; a.k_hs = k_hs; a.k_rs = k_rs;
+  a.V = V; a.v_hs = v_hs; a.v_rs = v_rs;
+  a.scale = scale; a.nnz = rem_nnz;
+  a.O = O; a.o_hs = o_hs; a.o_rs = o_rs;
+  a.Opart = t.Opart;
+  a.ml = t.ml;
+  return launch_attn<16, false>(a, st);
 }

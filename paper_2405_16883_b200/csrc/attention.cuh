@@ -33,6 +33,8 @@ struct AttnArgs {
   float* P;                // [H][nnz] nullable
   float* O;                // [H][M][d]
   long long o_hs, o_rs;
+  const float* Opart;      // optional [H][M][d] unnormalised partial (dense tiles), d == 64
+  const float2* ml;        // optional [H][M] running (max, sum) of the partial
 };
 
 // v[i] over lanes -> lane l holds sum over the group of the partials for entry l.
@@ -128,6 +130,12 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
   const int start = a.rowptr[row], end = a.rowptr[row + 1];
   float run_max = -INFINITY, run_sum = 0.f;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (a.Opart) {  // continue the online softmax of the dense-tile pass
+    const float2 mlv = a.ml[(long long)h * a.m + row];
+    run_max = mlv.x;
+    run_sum = mlv.y;
+    o = *reinterpret_cast<const float4*>(a.Opart + ((long long)h * a.m + row) * 64 + lane * 4);
+  }
   for (int base = start; base < end; base += G) {
     const int n = min(G, end - base);
     const int my_col = (lane < n) ? ld_stream(a.colidx + base + lane) : 0;
@@ -152,8 +160,8 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     }
     const float bmax = group_max<G>(s, mask);
     const float new_max = fmaxf(run_max, bmax);
-    const float p = (lane < n) ? expf(s - new_max) : 0.f;
-    const float corr = expf(run_max - new_max);  // 0 on the first batch (run_max = -inf)
+    const float p = (lane < n && s != -INFINITY) ? expf(s - new_max) : 0.f;
+    const float corr = (new_max == -INFINITY) ? 1.f : expf(run_max - new_max);
     run_sum = run_sum * corr + group_sum<G>(p, mask);
     o.x *= corr; o.y *= corr; o.z *= corr; o.w *= corr;
 #pragma unroll

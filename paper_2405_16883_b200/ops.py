@@ -317,6 +317,89 @@ def segment_softmax_(rowptr: torch.Tensor, vals: torch.Tensor) -> torch.Tensor:
     return vals
 
 
+TILE = 64              # rows per block / columns per tile of the tiled attention path
+TILE_MIN_FILL = 1 / 8  # a (block, tile) is dense when it holds at least this share of its slots
+TILE_MAX_PER_BLOCK = 8
+
+
+@dataclass
+class AttentionTilePlan:
+    """Dense 64x64 mask tiles (+ their values, NaN = absent) and the CSR remainder."""
+
+    tile_cols: torch.Tensor   # int32 [n_blocks, dt_max], -1 padded
+    tile_vals: torch.Tensor   # float32 [n_blocks, dt_max, 64, 64]
+    rem_rowptr: torch.Tensor  # int32 [m + 1]
+    rem_colidx: torch.Tensor  # int32 [rem_nnz]
+    rem_vals: torch.Tensor    # float32 [rem_nnz]
+    dense_share: float        # fraction of stored entries covered by dense tiles
+
+
+def attention_tile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, maskvals: torch.Tensor | None,
+                        n_cols: int, min_fill: float = TILE_MIN_FILL,
+                        max_tiles: int = TILE_MAX_PER_BLOCK) -> AttentionTilePlan | None:
+    """Plan-time split of a mask into dense 64x64 tiles and a remainder (None if no tile is dense)."""
+    require_cuda(rowptr, colidx)
+    dev = rowptr.device
+    m = rowptr.numel() - 1
+    nnz = colidx.numel()
+    if m == 0 or nnz == 0:
+        return None
+    vals = maskvals if maskvals is not None else torch.ones(nnz, dtype=torch.float32, device=dev)
+    rows = torch.repeat_interleave(torch.arange(m, device=dev), (rowptr[1:] - rowptr[:-1]).long())
+    cols = colidx.long()
+    nb, nt = -(-m // TILE), -(-n_cols // TILE)
+    blk, tc = rows // TILE, cols // TILE
+    counts = torch.bincount(blk * nt + tc, minlength=nb * nt).reshape(nb, nt)
+    score = torch.where(counts >= min_fill * TILE * TILE, counts, torch.zeros_like(counts))
+    dt = int(min(int((score > 0).sum(1).max().item()), max_tiles))
+    if dt == 0:
+        return None
+    top = torch.topk(score, dt, dim=1)
+    valid = top.values > 0
+    tsel = torch.where(valid, top.indices, torch.full_like(top.indices, nt))  # invalid sort last
+    tsel, order = torch.sort(tsel, dim=1)
+    valid = torch.gather(valid, 1, order)
+    tile_cols = torch.where(valid, tsel, torch.full_like(tsel, -1)).to(torch.int32)
+    slot = torch.full((nb, nt + 1), -1, dtype=torch.long, device=dev)
+    bidx = torch.arange(nb, device=dev)[:, None].expand(nb, dt)
+    slot[bidx[valid], tsel[valid]] = torch.arange(dt, device=dev)[None, :].expand(nb, dt)[valid]
+    s_e = slot[blk, tc]
+    inside = s_e >= 0
+    tile_vals = torch.full((nb, dt, TILE, TILE), float("nan"), dtype=torch.float32, device=dev)
+    tile_vals[blk[inside], s_e[inside], rows[inside] % TILE, cols[inside] % TILE] = vals[inside]
+    keep = ~inside
+    rem_rowptr = torch.zeros(m + 1, dtype=torch.long, device=dev)
+    rem_rowptr[1:] = torch.cumsum(torch.bincount(rows[keep], minlength=m), 0)
+    return AttentionTilePlan(tile_cols.contiguous(), tile_vals.contiguous(), rem_rowptr.to(torch.int32),
+                             colidx[keep].contiguous(), vals[keep].contiguous(),
+                             float(inside.sum().item()) / nnz)
+
+
+def sparse_attention_tiled(plan: AttentionTilePlan, Q, K, V, *, scale: float | None = None,
+                           workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Block-tiled fused attention (head dim 64): dense tiles on CUDA cores + remainder."""
+    require_cuda(Q, K, V)
+    squeeze = Q.dim() == 2
+    Q3, qhs, qrs = _head_view(_f32(Q), "Q")
+    K3, khs, krs = _head_view(_f32(K), "K")
+    V3, vhs, vrs = _head_view(_f32(V), "V")
+    H, m, d = Q3.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    nb, dt = plan.tile_cols.shape
+    if workspace is None:
+        nbytes = int(lib().stc_attention_tiled_workspace_bytes(m, H))
+        workspace = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=Q.device)
+    O = torch.empty((H, m, d), dtype=torch.float32, device=Q.device)
+    rc = lib().stc_sparse_attention_tiled_f32(
+        m, K3.shape[1], d, H, nb, dt, ptr(plan.tile_cols), ptr(plan.tile_vals), ptr(plan.rem_rowptr),
+        ptr(plan.rem_colidx), ptr(plan.rem_vals), plan.rem_colidx.numel(), ptr(Q3), qhs, qrs, ptr(K3), khs, krs,
+        ptr(V3), vhs, vrs, float(scale), ptr(O), O.stride(0), O.stride(1), ptr(workspace), workspace.numel() * 4,
+        stream_handle())
+    check(rc, "stc_sparse_attention_tiled_f32")
+    return O[0] if squeeze else O
+
+
 def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | None = None,
                      return_probs: bool = False):
     """Fused ``O = softmax_rows(scale * M .* QK^T) V``; optionally also S and P [H, nnz]."""

@@ -66,6 +66,14 @@ def sparse_attention(Q, K, V, mask: Tensor, scale: float | None = None, return_p
     d = Qt.shape[-1]
     if scale is None:
         scale = 1.0 / math.sqrt(d)
+    if not return_probs and d == ops.TILE:
+        # masks with dense bands (local windows) take the block-tiled kernel
+        key = ("attention_tile_plan",)
+        if key not in mask._cache:
+            mask._cache[key] = ops.attention_tile_plan(L.pos, L.crd, mask.storage.values, mask.shape[1])
+        plan = mask._cache[key]
+        if plan is not None and plan.dense_share >= 0.25:
+            return ops.sparse_attention_tiled(plan, Qt, Kt, Vt, scale=scale)
     res = ops.sparse_attention(L.pos, L.crd, Qt, Kt, Vt, maskvals=mask.storage.values, scale=scale,
                                return_probs=return_probs)
     if not return_probs:

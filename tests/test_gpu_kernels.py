@@ -212,3 +212,24 @@ def test_coo_segments_and_mttkrp():
             got = ops.mttkrp_coo3(seg, Jt, Kt, Vt, torch.from_numpy(B[:, :R].copy()).cuda(),
                                   torch.from_numpy(C[:, :R].copy()).cuda(), variant=variant).cpu().numpy()
             assert parity_gate(got, want[:, :R], want[:, :R], TOL)[0]
+
+
+@pytest.mark.parametrize("seq,window,nrand,heads", [(200, 40, 8, 2), (700, 256, 64, 1), (130, 300, 5, 3)])
+def test_tiled_attention_matches_oracle(seq, window, nrand, heads):
+    from paper_2405_16883_b200 import synthetic
+
+    M, Q, K, V = synthetic.cfg4(seq=seq, heads=heads, dim=64, window=window, n_random=nrand)
+    rng = np.random.default_rng(seq)
+    mv = np.where(rng.random(M.nnz) < 0.1, 0.0, rng.uniform(0.5, 2.0, M.nnz)).astype(np.float32)  # incl. zeros
+    R, Cc, MV = dev(M.rowptr, M.colidx, mv)
+    plan = ops.attention_tile_plan(R, Cc, MV, seq)
+    assert plan is not None and plan.dense_share > 0.3
+    Qt, Kt, Vt = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+    O = ops.sparse_attention_tiled(plan, Qt, Kt, Vt, scale=0.125).cpu().numpy()
+    for h in range(heads):
+        s = 0.125 * native.sddmm_csr(M.rowptr, M.colidx, mv, Q[h], K[h])
+        p = native.segment_softmax(M.rowptr, s)
+        o = native.spmm_csr(M.rowptr, M.colidx, p, V[h])
+        ob = native.spmm_csr(M.rowptr, M.colidx, p, np.abs(V[h]))
+        ok, worst = parity_gate(O[h], o, ob, TOL)
+        assert ok, worst
