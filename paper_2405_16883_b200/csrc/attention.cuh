@@ -53,6 +53,27 @@ STC_DEVICE float transpose_reduce(float (&v)[G], int lane, unsigned mask) {
   return v[0];
 }
 
+// B partial sums over G lanes (B <= G, powers of two): lane l ends with the full
+// sum of entry l % B (transposed stages inside aligned groups of B lanes, then a
+// plain butterfly across the G / B groups).
+template <int B, int G>
+STC_DEVICE float transpose_reduce_b(float (&v)[B], int lane, unsigned mask) {
+#pragma unroll
+  for (int h = B / 2; h >= 1; h >>= 1) {
+    const bool upper = lane & h;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = upper ? v[i] : v[i + h];
+      const float keep = upper ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(mask, send, h, G);
+    }
+  }
+  float x = v[0];
+#pragma unroll
+  for (int h = B; h < G; h <<= 1) x += __shfl_xor_sync(mask, x, h, G);
+  return x;
+}
+
 template <int G>
 STC_DEVICE float group_max(float x, unsigned mask) {
 #pragma unroll
@@ -117,8 +138,11 @@ __global__ void __launch_bounds__(256) segsoftmax_kernel(int m, long long nnz, c
 }
 
 // Fused: O[h,i,:] = sum_j softmax_j(scale * m_ij * q_i.k_j) * v_j with an online softmax.
+// Entries are consumed in batches of B <= G (B = G/2 for wide heads keeps the
+// V-row registers small enough for two CTAs' worth of extra warps per SM).
 template <int G, bool WRITE_S>
 __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
+  constexpr int B = G >= 16 ? G / 2 : G;
   const int lane = threadIdx.x % G;
   const unsigned mask = subwarp_mask<G>();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -136,13 +160,14 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     run_sum = mlv.y;
     o = *reinterpret_cast<const float4*>(a.Opart + ((long long)h * a.m + row) * 64 + lane * 4);
   }
-  for (int base = start; base < end; base += G) {
-    const int n = min(G, end - base);
-    const int my_col = (lane < n) ? ld_stream(a.colidx + base + lane) : 0;
-    float part[G];
-    float4 vv[G];
+  int next_col = (start + lane < end && lane < B) ? ld_stream(a.colidx + start + lane) : 0;
+  for (int base = start; base < end; base += B) {
+    const int n = min(B, end - base);
+    const int my_col = next_col;
+    float part[B];
+    float4 vv[B];
 #pragma unroll
-    for (int t = 0; t < G; ++t) {
+    for (int t = 0; t < B; ++t) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
       vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -152,20 +177,24 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
       }
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
-    float s = transpose_reduce<G>(part, lane, mask);
-    const float mv = (lane < n && a.maskv) ? ld_stream(a.maskv + base + lane) : 1.f;
-    s = (lane < n) ? s * mv * a.scale : -INFINITY;
+    // indices of the next batch stream in while this one is reduced
+    next_col = (base + B + lane < end && lane < B) ? ld_stream(a.colidx + base + B + lane) : 0;
+    float s = transpose_reduce_b<B, G>(part, lane, mask);
+    const bool mine = (lane % B) < n;  // lane l carries entry l % B
+    const float mv = (mine && a.maskv) ? ld_stream(a.maskv + base + lane % B) : 1.f;
+    s = mine ? s * mv * a.scale : -INFINITY;
     if constexpr (WRITE_S) {
       if (lane < n) a.S[h * a.nnz + base + lane] = s;
     }
     const float bmax = group_max<G>(s, mask);
     const float new_max = fmaxf(run_max, bmax);
-    const float p = (lane < n && s != -INFINITY) ? expf(s - new_max) : 0.f;
+    const float p = (mine && s != -INFINITY) ? expf(s - new_max) : 0.f;
     const float corr = (new_max == -INFINITY) ? 1.f : expf(run_max - new_max);
-    run_sum = run_sum * corr + group_sum<G>(p, mask);
+    // each entry appears in G / B lanes: count it once in the sum
+    run_sum = run_sum * corr + group_sum<G>(lane < B ? p : 0.f, mask);
     o.x *= corr; o.y *= corr; o.z *= corr; o.w *= corr;
 #pragma unroll
-    for (int t = 0; t < G; ++t) {
+    for (int t = 0; t < B; ++t) {
       const float pt = __shfl_sync(mask, p, t, G);
       o.x = fmaf(pt, vv[t].x, o.x);
       o.y = fmaf(pt, vv[t].y, o.y);
@@ -181,8 +210,8 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     // P = exp(S - max) / sum, from the scores this group just wrote (parity mode)
     if (a.P) {
       __syncwarp(mask);
-      for (int p = start + lane; p < end; p += G)
-        a.P[h * a.nnz + p] = expf(a.S[h * a.nnz + p] - run_max) * inv;
+      for (int pp = start + lane; pp < end; pp += G)
+        a.P[h * a.nnz + pp] = expf(a.S[h * a.nnz + pp] - run_max) * inv;
     }
   }
 }

@@ -54,8 +54,10 @@ __global__ void __launch_bounds__(AT_THREADS, 3) attn_tile_kernel(TileArgs a) {
   const float* Kh = a.K + h * a.k_hs;
   const float* Vh = a.V + h * a.v_hs;
 
+  // lanes walk rows (consecutive r) for a fixed d-quad, so the transposed
+  // scalar stores hit 32 distinct banks
   for (int idx = tid; idx < AT_B * (AT_D / 4); idx += AT_THREADS) {
-    const int r = idx / (AT_D / 4), dq = (idx % (AT_D / 4)) * 4;
+    const int r = idx % AT_B, dq = (idx / AT_B) * 4;
     float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
     if (row0 + r < a.m) q = *reinterpret_cast<const float4*>(Qh + (long long)(row0 + r) * a.q_rs + dq);
     Qt[(dq + 0) * AT_B + r] = q.x;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(AT_THREADS, 3) attn_tile_kernel(TileArgs a) {
     __syncthreads();  // previous tile's operands fully consumed
     const int c0 = tc * AT_B;
     for (int idx = tid; idx < AT_B * (AT_D / 4); idx += AT_THREADS) {
-      const int c = idx / (AT_D / 4), dq = (idx % (AT_D / 4)) * 4;
+      const int c = idx % AT_B, dq = (idx / AT_B) * 4;
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f), vv = kv;
       if (c0 + c < a.n) {
         kv = ld_gather4(Kh + (long long)(c0 + c) * a.k_rs + dq);
@@ -140,13 +142,18 @@ __global__ void __launch_bounds__(AT_THREADS, 3) attn_tile_kernel(TileArgs a) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[i][e] *= corr;
     }
+    // P^T in SMEM, float4 slot of rows 4ty.. in column c swizzled to ty ^ ((c >> 2) & 7):
+    // conflict-free stores here and broadcast loads in the PV loop
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<float4*>(Pt + (4 * tx + j) * AT_B + 4 * ty) = make_float4(p[0][j], p[1][j], p[2][j], p[3][j]);
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * tx + j;
+      *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * (ty ^ ((c >> 2) & 7))) =
+          make_float4(p[0][j], p[1][j], p[2][j], p[3][j]);
+    }
     __syncthreads();
 #pragma unroll 8
     for (int c = 0; c < AT_B; ++c) {
-      const float4 p4 = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * ty);
+      const float4 p4 = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ ((c >> 2) & 7)));
       const float4 v4 = *reinterpret_cast<const float4*>(Vs + c * AT_D + 4 * tx);
       const float pa[4] = {p4.x, p4.y, p4.z, p4.w};
       const float va[4] = {v4.x, v4.y, v4.z, v4.w};
