@@ -47,6 +47,7 @@ struct SpmmOp {
   unsigned lane_off = 0;  // this lane's first column (added in 32-bit)
 
   static constexpr int kRing = 8;           // gathers in flight per group
+  static constexpr int kMinBlocks = 4;      // resident CTAs per SM (register budget)
   static constexpr int kStageBytes = 32768;  // staged items per CTA (rest of SMEM stays L1)
   struct Item {
     unsigned off;
@@ -57,7 +58,8 @@ struct SpmmOp {
   struct Pre {
     Frag<VEC> b;
   };
-  STC_DEVICE Item load(long long p) const {
+  struct State {};
+  STC_DEVICE Item load(long long p, bool /*first*/) const {
     return Item{(unsigned)((long long)ld_stream(col + p) * ldb), ld_stream(val + p)};
   }
   STC_DEVICE static Item dummy() { return Item{0u, 0.f}; }
@@ -67,10 +69,12 @@ struct SpmmOp {
   }
   STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
   STC_DEVICE void fetch(const Item& it, Pre& pre) const { pre.b.load_gather(B + (it.off + lane_off)); }
-  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre, const Item& it) const {
+  STC_DEVICE void accumulate(Frag<VEC>& acc, State&, const Pre& pre, const Item& it) const {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v, pre.b.v[e], acc.v[e]);
   }
+  STC_DEVICE static void init(State&) {}
+  STC_DEVICE static void finish(Frag<VEC>&, State&) {}
 };
 
 template <int VEC>
@@ -84,35 +88,66 @@ struct MttkrpOp {
   long long ldcf;
   unsigned lane_off = 0;
 
+  // Fiber factorisation: entries are sorted by (i, j), so consecutive entries of
+  // one (i, j) fiber share B[j,:]. M[i,:] += B[j,:] * sum_k T[i,j,k] C[k,:] gathers
+  // B[j,:] once per fiber (flag = first entry of a fiber) instead of once per entry.
   static constexpr int kRing = VEC == 4 ? 4 : 8;
-  static constexpr int kStageBytes = 16384;  // small: the hot factor rows live in L1
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kStageBytes = 32768;  // 3 CTAs x 50 KB SMEM leaves ~75 KB of L1 for the hot factor rows
   struct __align__(16) Item {
     unsigned offb, offc;
     float v;
-    float pad;
+    int flag;  // 1: first entry of a fiber (j differs from the previous entry's)
   };
   struct Pre {
     Frag<VEC> b, c;
   };
-  STC_DEVICE Item load(long long p) const {
-    return Item{(unsigned)((long long)ld_stream(jc + p) * ldb), (unsigned)((long long)ld_stream(kc + p) * ldcf),
-                ld_stream(val + p), 0.f};
+  struct State {
+    Frag<VEC> b, f;  // the open fiber's B[j,:] and its running sum_k T C[k,:]
+    bool open;
+  };
+  STC_DEVICE Item load(long long p, bool first) const {
+    const int j = ld_stream(jc + p);
+    const bool start = first || p == 0 || ld_stream(jc + p - 1) != j;
+    return Item{(unsigned)((long long)j * ldb), (unsigned)((long long)ld_stream(kc + p) * ldcf), ld_stream(val + p),
+                start ? 1 : 0};
   }
-  STC_DEVICE static Item dummy() { return Item{0u, 0u, 0.f, 0.f}; }
+  STC_DEVICE static Item dummy() { return Item{0u, 0u, 0.f, 0}; }
   template <int SUBW>
   STC_DEVICE Item shfl(const Item& it, int src, unsigned mask) const {
     return Item{__shfl_sync(mask, it.offb, src, SUBW), __shfl_sync(mask, it.offc, src, SUBW),
-                __shfl_sync(mask, it.v, src, SUBW), 0.f};
+                __shfl_sync(mask, it.v, src, SUBW), __shfl_sync(mask, it.flag, src, SUBW)};
   }
   STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
-    pre.b.load_gather(B + (it.offb + lane_off));
+    if (it.flag) pre.b.load_gather(B + (it.offb + lane_off));
     pre.c.load_gather(C + (it.offc + lane_off));
   }
-  STC_DEVICE void accumulate(Frag<VEC>& acc, const Pre& pre, const Item& it) const {
-    // reference term order: (t * B[j,r]) * C[k,r]  (engine.py:394-402)
+  STC_DEVICE static void init(State& st) {
+    st.b.zero();
+    st.f.zero();
+    st.open = false;
+  }
+  STC_DEVICE void accumulate(Frag<VEC>& acc, State& st, const Pre& pre, const Item& it) const {
+    const bool close = it.flag && st.open;
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v * pre.b.v[e], pre.c.v[e], acc.v[e]);
+    for (int e = 0; e < VEC; ++e) {
+      const float t = fmaf(st.b.v[e], st.f.v[e], acc.v[e]);
+      acc.v[e] = close ? t : acc.v[e];
+      st.f.v[e] = it.flag ? 0.f : st.f.v[e];
+      st.b.v[e] = it.flag ? pre.b.v[e] : st.b.v[e];
+      st.f.v[e] = fmaf(it.v, pre.c.v[e], st.f.v[e]);
+    }
+    st.open = true;
+  }
+  // close the open fiber into `acc` before `acc` is written out
+  STC_DEVICE static void finish(Frag<VEC>& acc, State& st) {
+    if (st.open) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(st.b.v[e], st.f.v[e], acc.v[e]);
+      st.f.zero();
+      st.open = false;
+    }
   }
 };
 
@@ -196,18 +231,31 @@ __host__ __device__ constexpr int merge_rows_cap() {
 }
 constexpr int kStagePad = 8;  // dummy items after each window: branch-free prefetch
 
+// Per-group strides of the staged windows, skewed so that the groups of one warp
+// (which read different items in the same instruction) start in different banks.
+__host__ __device__ constexpr int bank_skewed(int n, int elem_bytes) {
+  const int per_line = 128 / elem_bytes;  // elements per 128-byte bank line
+  return n + ((1 - n % per_line) + per_line) % per_line;
+}
+template <int SUBW, class Op>
+__host__ __device__ constexpr int merge_item_stride() {
+  return bank_skewed(merge_stage_cap<SUBW, Op>() + kStagePad, (int)sizeof(typename Op::Item));
+}
+template <int SUBW, class Op>
+__host__ __device__ constexpr int merge_rend_stride() {
+  return bank_skewed(merge_rows_cap<SUBW, Op>(), (int)sizeof(int));
+}
+
 // Dynamic shared memory of merge_kernel (independent of ipg: groups stream
 // their items through a fixed-size window).
 template <int SUBW, int VEC, class Op>
 __host__ __device__ constexpr size_t merge_smem_bytes() {
   constexpr int NG = 256 / SUBW;
   constexpr int SW = SUBW * VEC;
-  constexpr int CAP = merge_stage_cap<SUBW, Op>();
-  constexpr int CAPR = merge_rows_cap<SUBW, Op>();
   return (size_t)2 * NG * SW * sizeof(float)               // head / tail partials
          + (size_t)2 * NG * sizeof(int)                     // their row ids
-         + (size_t)NG * (CAP + kStagePad) * sizeof(typename Op::Item)  // staged items window
-         + (size_t)NG * CAPR * sizeof(int);                 // staged row-end window
+         + (size_t)NG * merge_item_stride<SUBW, Op>() * sizeof(typename Op::Item)  // staged items window
+         + (size_t)NG * merge_rend_stride<SUBW, Op>() * sizeof(int);                // staged row-end window
 }
 
 // One sub-warp ("group") per `ipg` merge items. The group stages a window of
@@ -217,7 +265,7 @@ __host__ __device__ constexpr size_t merge_smem_bytes() {
 // accumulated, independent of row boundaries, so U loads stay in flight
 // across rows.
 template <int SUBW, int VEC, int EPI, bool ADD, int U, bool FULL, class Op>
-__global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, Op op) {
+__global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, MergeShape ms, Op op) {
   static_assert(U <= kStagePad, "ring deeper than the staging pad");
   using Item = typename Op::Item;
   constexpr int NG = 256 / SUBW;
@@ -230,7 +278,9 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
   int* Hrow = reinterpret_cast<int*>(Ts + NG * SW);                     // [NG]
   int* Trow = Hrow + NG;                                                // [NG]
   Item* items_all = reinterpret_cast<Item*>(Trow + NG);                 // [NG][CAP]
-  int* rend_all = reinterpret_cast<int*>(items_all + NG * (CAP + kStagePad));  // [NG][CAPR]
+  constexpr int IST = merge_item_stride<SUBW, Op>();
+  constexpr int RST = merge_rend_stride<SUBW, Op>();
+  int* rend_all = reinterpret_cast<int*>(items_all + NG * IST);         // [NG][RST]
 
   const int sub = threadIdx.x / SUBW;
   const int lane = threadIdx.x % SUBW;
@@ -240,8 +290,8 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
   const int z = blockIdx.z;
   const int col0 = slab * SW + lane * VEC;
   const bool col_ok = FULL || col0 < o.k;
-  Item* items = items_all + sub * (CAP + kStagePad);
-  int* rend = rend_all + sub * CAPR;
+  Item* items = items_all + sub * IST;
+  int* rend = rend_all + sub * RST;
 
   if (z) {
     op.val += z * ms.batch_val_stride;
@@ -282,8 +332,11 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
   int cur_start = first_start - s.y;                 // relative start (may be negative)
   Frag<VEC> acc;
   acc.zero();
+  typename Op::State fst;
+  Op::init(fst);
 
   auto flush = [&]() {
+    Op::finish(acc, fst);
     const int row = row0 + r;
     if (r == 0 && head_mid) {
       if (col_ok) acc.store_plain(&Hs[sub * SW + lane * VEC]);
@@ -305,7 +358,7 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
   for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
     const int wn = min(CAP, n_nnz - w0);
     __syncwarp(mask);
-    for (int t = lane; t < wn + kStagePad; t += SUBW) items[t] = t < wn ? op.load(s.y + w0 + t) : Op::dummy();
+    for (int t = lane; t < wn + kStagePad; t += SUBW) items[t] = t < wn ? op.load(s.y + w0 + t, w0 + t == 0) : Op::dummy();
     __syncwarp(mask);
     int end_w = cur_end - w0;  // current row's end, relative to the window
 #pragma unroll
@@ -319,7 +372,7 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
           flush();
           end_w = cur_end - w0;
         }
-        op.accumulate(acc, ring[u], items[q0 + u]);
+        op.accumulate(acc, fst, ring[u], items[q0 + u]);
         if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
       }
     }
@@ -330,11 +383,12 @@ __global__ void __launch_bounds__(256, 4) merge_kernel(SegOut o, MergeShape ms, 
           flush();
           end_w = cur_end - w0;
         }
-        op.accumulate(acc, ring[u], items[q0 + u]);
+        op.accumulate(acc, fst, ring[u], items[q0 + u]);
       }
     }
   }
   while (r < n_rows) flush();
+  Op::finish(acc, fst);
   if (row0 + r < o.m && n_nnz > cur_start && r == n_rows) {
     if (col_ok) acc.store_plain(&Ts[sub * SW + lane * VEC]);
     if (lane == 0) Trow[sub] = row0 + r;
@@ -482,9 +536,11 @@ __global__ void __launch_bounds__(256) row_kernel(SegOut o, MergeShape ms, Op op
   const int end = o.rowptr[row + 1];
   Frag<VEC> acc;
   acc.zero();
+  typename Op::State fst;
+  Op::init(fst);
   for (int base = start; base < end; base += SUBW) {
     typename Op::Item it{};
-    if (base + lane < end) it = op.load(base + lane);
+    if (base + lane < end) it = op.load(base + lane, base + lane == start);
     const int n = min(SUBW, end - base);
     for (int q0 = 0; q0 < n; q0 += U) {
       typename Op::Pre pre[U];
@@ -496,9 +552,10 @@ __global__ void __launch_bounds__(256) row_kernel(SegOut o, MergeShape ms, Op op
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (q0 + u < n) op.accumulate(acc, pre[u], iu[u]);
+        if (q0 + u < n) op.accumulate(acc, fst, pre[u], iu[u]);
     }
   }
+  Op::finish(acc, fst);
   if (col_ok) write_row<VEC, EPI, ADD>(o, row, col0, acc);
 }
 
