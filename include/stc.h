@@ -49,6 +49,9 @@ extern "C" {
 #define STC_EPILOGUE_NONE 0
 #define STC_EPILOGUE_RELU 1
 
+#define STC_EWISE_UNION 0     /* C = A + B over the union of patterns        */
+#define STC_EWISE_INTERSECT 1 /* C = A .* B over the intersection            */
+
 int stc_abi_version(void);
 const char* stc_last_error(void);
 
@@ -172,7 +175,8 @@ int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, int n_blocks,
                                    long long o_rs, void* ws, size_t ws_bytes, void* stream);
 
 /* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
- * M[s,:] = sum_{p in seg s} (vals[p] * B[j[p],:]) * C[k[p],:]
+ * M[s,:] = sum_{p in seg s} vals[p] * B[j[p],:] * C[k[p],:], evaluated fiber by
+ * fiber: each run of equal j sums vals * C[k,:] and multiplies by B[j,:] once.
  * B has n_j rows, C has n_k rows (each below 2^32 elements: 32-bit gather offsets).
  * Replaces `_run_sparse_output` with the (i,r) Workspace, engine.py:577-644,
  * 71-90, for M(i,r) = T(i,j,k) * B(j,r) * C(k,r).                           */
@@ -181,6 +185,41 @@ int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd
                         int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
                         const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                         void* stream);
+
+/* ---- sparse x sparse on CSR operands ------------------
+ * SpGEMM C(i,k) = A(i,j) * B(j,k), CSR x CSR -> CSR, replacing the reference's
+ * workspace plan ([i,j,k], Workspace over k: engine.py:577-644, 71-90). Output
+ * structure = every (i,k) reached by a product (arithmetic zeros are kept);
+ * values = 0.0 + a_ij1*b_j1k + a_ij2*b_j2k + ... in ascending j (fp32).
+ * Three phases, sizes read back by the caller between them:
+ *   1. stc_spgemm_products: prod_ptr[m+1] = exclusive scan of per-row product
+ *      counts; products = prod_ptr[m] (temp: stc_spgemm_products_temp_bytes).
+ *   2. stc_spgemm_symbolic: expands and sorts the products into `ws`
+ *      (stc_spgemm_workspace_bytes(m, products)) and writes c_rowptr[m+1].
+ *   3. stc_spgemm_numeric: c_colidx / c_vals (c_rowptr[m] entries) from `ws`. */
+size_t stc_spgemm_products_temp_bytes(int m);
+int stc_spgemm_products(int m, const int* a_rowptr, const int* a_colidx, const int* b_rowptr,
+                        long long* prod_ptr, void* temp, size_t temp_bytes, void* stream);
+size_t stc_spgemm_workspace_bytes(int m, long long products);
+int stc_spgemm_symbolic(int m, int n, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+                        const int* b_rowptr, const int* b_colidx, const float* b_vals,
+                        const long long* prod_ptr, long long products, void* ws, size_t ws_bytes,
+                        int* c_rowptr, void* stream);
+int stc_spgemm_numeric(int m, long long products, void* ws, size_t ws_bytes, const int* c_rowptr,
+                       int* c_colidx, float* c_vals, void* stream);
+
+/* Element-wise CSR (same shape): STC_EWISE_UNION C = A + B (two terms, the
+ * reference's _union_sorted, engine.py:224-230; value (0 + a) + b, or 0 + a /
+ * 0 + b where only one side stores the coordinate), STC_EWISE_INTERSECT
+ * C = A .* B (_intersect_sorted, engine.py:208-221; value 0 + a * b).
+ * stc_csr_ewise_symbolic writes c_rowptr[m+1] (temp: stc_csr_ewise_temp_bytes);
+ * stc_csr_ewise_f32 fills c_colidx / c_vals.                                  */
+size_t stc_csr_ewise_temp_bytes(int m);
+int stc_csr_ewise_symbolic(int op, int m, const int* a_rowptr, const int* a_colidx, const int* b_rowptr,
+                           const int* b_colidx, int* c_rowptr, void* temp, size_t temp_bytes, void* stream);
+int stc_csr_ewise_f32(int op, int m, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+                      const int* b_rowptr, const int* b_colidx, const float* b_vals, const int* c_rowptr,
+                      int* c_colidx, float* c_vals, void* stream);
 
 #ifdef __cplusplus
 }

@@ -169,6 +169,78 @@ def mttkrp_abs(i, j, k, vals, B, C):
     return mttkrp_coo(i, j, k, np.abs(vals), np.abs(B), np.abs(C))
 
 
+def spgemm_csr(ap, aj, av, bp, bj, bv):
+    """C = A @ B for CSR A, CSR B -> CSR (rowptr, colidx, vals).
+
+    Reference: `_run_sparse_output` with the [i, j, k] plan and a Workspace over
+    k (engine.py:577-644, 71-90): for each row i, j ascending over A's row, k
+    ascending over B's row j, ``ws[k] = ws.get(k, 0.0) + a_ij * b_jk``; the
+    drain emits every touched k in order, zeros included. Vectorised as an
+    expansion in (i, j, k) order, a stable sort by (i, k), and run sums from
+    0.0 (``np.add.reduceat`` would pair-sum, so runs are folded position-major).
+    """
+    ap, aj, bp, bj = (np.asarray(x, dtype=np.int64) for x in (ap, aj, bp, bj))
+    av, bv = np.asarray(av, dtype=np.float64), np.asarray(bv, dtype=np.float64)
+    m = len(ap) - 1
+    a_rows = np.repeat(np.arange(m), np.diff(ap))
+    blen = np.diff(bp)[aj]
+    # expand: product t belongs to A entry e = rep[t], B position bp[aj[e]] + offset
+    rep = np.repeat(np.arange(len(aj)), blen)
+    first = np.repeat(np.cumsum(blen) - blen, blen)
+    bpos = bp[aj][rep] + (np.arange(len(rep)) - first)
+    rows = a_rows[rep]
+    keys = bj[bpos]
+    prod = av[rep] * bv[bpos]
+    order = np.lexsort((keys, rows))  # stable: equal (i, k) keep ascending j
+    rows, keys, prod = rows[order], keys[order], prod[order]
+    newrun = np.ones(len(keys), dtype=bool)
+    newrun[1:] = (rows[1:] != rows[:-1]) | (keys[1:] != keys[:-1])
+    run_id = np.cumsum(newrun) - 1
+    n_out = int(newrun.sum())
+    vals = np.zeros(n_out, dtype=np.float64)
+    starts = np.flatnonzero(newrun)
+    lens = np.diff(np.append(starts, len(keys)))
+    for p in range(int(lens.max()) if n_out else 0):
+        live = np.flatnonzero(lens > p)
+        vals[live] = vals[live] + prod[starts[live] + p]
+    del run_id
+    out_rows = rows[starts]
+    rowptr = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(rowptr, out_rows + 1, 1)
+    return np.cumsum(rowptr), keys[starts], vals
+
+
+def csr_ewise(op, ap, aj, av, bp, bj, bv):
+    """Element-wise CSR: ``op="add"`` (union; value (0.0 + a) + b, or the one present
+    side plus 0.0) or ``op="mul"`` (intersection; value 0.0 + a * b).
+
+    Reference: the two-term union / one-term intersection co-iteration of
+    `_run_sparse_output` (engine.py:608-633, `_union_sorted` :224-230,
+    `_intersect_sorted` :208-221) with a Workspace slot starting at 0.0 and the
+    terms accumulated in expression order (engine.py:594-604).
+    """
+    ap, aj, bp, bj = (np.asarray(x, dtype=np.int64) for x in (ap, aj, bp, bj))
+    av, bv = np.asarray(av, dtype=np.float64), np.asarray(bv, dtype=np.float64)
+    m = len(ap) - 1
+    n = int(max(aj.max(initial=-1), bj.max(initial=-1))) + 1
+    ka = np.repeat(np.arange(m), np.diff(ap)) * n + aj
+    kb = np.repeat(np.arange(m), np.diff(bp)) * n + bj
+    if op == "mul":
+        keys, ia, ib = np.intersect1d(ka, kb, assume_unique=True, return_indices=True)
+        vals = 0.0 + av[ia] * bv[ib]
+    else:
+        keys = np.union1d(ka, kb)
+        vals = np.zeros(len(keys), dtype=np.float64)
+        pa = np.searchsorted(keys, ka)
+        vals[pa] = vals[pa] + av
+        pb = np.searchsorted(keys, kb)
+        vals[pb] = vals[pb] + bv
+    rows = keys // max(n, 1)
+    rowptr = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(rowptr, rows + 1, 1)
+    return np.cumsum(rowptr), keys % max(n, 1), vals
+
+
 def relu(x):
     return np.maximum(np.asarray(x, dtype=np.float64), 0.0)
 

@@ -35,6 +35,9 @@ VARIANTS = {"row": VARIANT_ROW, "merge": VARIANT_MERGE, "coltile": VARIANT_COLTI
 EPILOGUE_NONE = 0
 EPILOGUE_RELU = 1
 
+EWISE_UNION = 0
+EWISE_INTERSECT = 1
+
 _p = ctypes.c_void_p
 _i = ctypes.c_int
 _ll = ctypes.c_longlong
@@ -70,6 +73,14 @@ SIGNATURES = {
                                             _ll, _p, _ll, _ll, _f, _p, _ll, _ll, _p, _sz, _p]),
     "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _i, _p, _i,
                                  _p, _sz, _p]),
+    "stc_spgemm_products_temp_bytes": (_sz, [_i]),
+    "stc_spgemm_products": (_i, [_i, _p, _p, _p, _p, _p, _sz, _p]),
+    "stc_spgemm_workspace_bytes": (_sz, [_i, _ll]),
+    "stc_spgemm_symbolic": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _p, _ll, _p, _sz, _p, _p]),
+    "stc_spgemm_numeric": (_i, [_i, _ll, _p, _sz, _p, _p, _p, _p]),
+    "stc_csr_ewise_temp_bytes": (_sz, [_i]),
+    "stc_csr_ewise_symbolic": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "stc_csr_ewise_f32": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
 }
 
 

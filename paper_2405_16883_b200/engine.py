@@ -17,6 +17,9 @@ A COO / DCSR / CSC (any storage order)                   [compressed, dense] + w
 ``Sc(h,i,j) = M(i,j)*Q(h,i,d)*K(h,j,d)``                 [dense,dense,compressed]    head-batched SDDMM
 ``O(h,i,d) = P(h,i,j)*V(h,j,d)``                         dense, [h,i,j,d], {d}       head-batched merge
 ``M(i,r) = T(i,j,k)*B(j,r)*C(k,r)``, T COO               [compressed, dense] + ws    MTTKRP merge
+``C(i,k) = A(i,j)*B(j,k)``, A and B CSR                  CSR, [i,j,k], ws {k}        SpGEMM (expand-sort-compress)
+``C(i,j) = A(i,j) + B(i,j)``, CSR                        CSR, [i,j] (union)          element-wise union
+``C(i,j) = A(i,j) * B(i,j)``, CSR                        CSR, [i,j] (intersection)   element-wise product
 all operands dense                                       dense dispatch              torch (cuBLAS, TF32 off)
 =====================================================  ==========================  ===================
 
@@ -693,6 +696,89 @@ def _exec_sparse_spmm(ctx: _Ctx, m: _SpmmTerm) -> Tensor:
     return _compressed_dense_result(ctx.expr.output_name, (view.n_rows, K), rows, Y)
 
 
+# ---------------------------------------------------------------------------
+# Sparse x sparse
+# ---------------------------------------------------------------------------
+
+
+def _is_csr(t: Tensor) -> bool:
+    f = t.format
+    return f.order == 2 and f.mode_ordering == (0, 1) and f.levels == (LevelFormat.DENSE, LevelFormat.COMPRESSED)
+
+
+def _csr_out(ctx: _Ctx, shape, r: ops.CsrResult) -> Tensor:
+    fmt = ctx.out_fmt
+    if fmt.order != 2 or fmt.mode_ordering != (0, 1) or fmt.levels != (LevelFormat.DENSE, LevelFormat.COMPRESSED):
+        raise UnsupportedExpressionError(
+            f"sparse x sparse into {fmt.name()} is not supported on the device (CSR output only)")
+    st = TensorStorage(fmt, (DenseLevel(shape[0]), CompressedLevel(r.rowptr, r.colidx)), r.vals)
+    return Tensor(ctx.expr.output_name, tuple(shape), st)
+
+
+@dataclass
+class _SpgemmTerm:
+    A: Access
+    B: Access
+
+
+def _match_spgemm(term, out_vars) -> _SpgemmTerm | None:
+    if len(term) != 2 or not all(a.tensor.format.has_sparse_levels and a.tensor.order == 2 for a in term):
+        return None
+    for A, B in ((term[0], term[1]), (term[1], term[0])):
+        i, j = A.indices
+        j2, k = B.indices
+        if j == j2 and len({i, j, k}) == 3 and list(out_vars) == [i, k]:
+            return _SpgemmTerm(A, B)
+    return None
+
+
+def _exec_spgemm(ctx: _Ctx, g: _SpgemmTerm) -> Tensor:
+    """Gustavson SpGEMM; counters of the reference's [i, j, k] workspace nest:
+    mults = adds = P (products), iterator advances = m + 2 nnz(A) + 2 P."""
+    A, B = ctx.t(g.A), ctx.t(g.B)
+    if not (_is_csr(A) and _is_csr(B)):
+        raise UnsupportedExpressionError("device SpGEMM needs CSR operands accessed in storage order")
+    la, lb = A.storage.levels[1], B.storage.levels[1]
+    r = ops.spgemm_csr(la.pos, la.crd, A.storage.values, lb.pos, lb.crd, B.storage.values)
+    ctx.chosen.append("spgemm:esc")
+    m, nnz_a = A.shape[0], int(A.storage.values.numel())
+    ctx.counter.add(r.products, r.products, m + 2 * nnz_a + 2 * r.products)
+    return _csr_out(ctx, (A.shape[0], B.shape[1]), r)
+
+
+def _match_ewise(terms, out_vars):
+    """("add", A, B) for A(i,j) + B(i,j); ("mul", A, B) for A(i,j) * B(i,j)."""
+    ov = tuple(out_vars)
+
+    def ok(a):
+        return a.tensor.format.has_sparse_levels and a.tensor.order == 2 and a.indices == ov
+    if len(terms) == 2 and all(len(t) == 1 and ok(t[0]) for t in terms):
+        return "add", terms[0][0], terms[1][0]
+    if len(terms) == 1 and len(terms[0]) == 2 and all(ok(a) for a in terms[0]):
+        return "mul", terms[0][0], terms[0][1]
+    return None
+
+
+def _exec_ewise(ctx: _Ctx, op: str, a: Access, b: Access) -> Tensor:
+    """Element-wise union / intersection; counters of the reference's co-iteration
+    (`_union_sorted` / `_intersect_sorted` over [i, j], engine.py:208-230, 577-644)."""
+    A, B = ctx.t(a), ctx.t(b)
+    if not (_is_csr(A) and _is_csr(B)):
+        raise UnsupportedExpressionError("device element-wise ops need CSR operands accessed in storage order")
+    la, lb = A.storage.levels[1], B.storage.levels[1]
+    r = ops.csr_ewise(op, la.pos, la.crd, A.storage.values, lb.pos, lb.crd, B.storage.values)
+    ctx.chosen.append(f"ewise:{op}")
+    m = A.shape[0]
+    nnz_a, nnz_b, nnz_c = int(A.storage.values.numel()), int(B.storage.values.numel()), int(r.vals.numel())
+    if op == "add":
+        ctx.counter.add(0, nnz_a + nnz_b, m + 2 * (nnz_a + nnz_b) + 2 * nnz_c)
+    else:
+        lens = torch.minimum(la.pos[1:] - la.pos[:-1], lb.pos[1:] - lb.pos[:-1]).long()
+        both = int((lens > 0).sum().item())
+        ctx.counter.add(nnz_c, nnz_c, m + int(lens.sum().item()) + both + 4 * nnz_c)
+    return _csr_out(ctx, A.shape, r)
+
+
 def _dispatch(ctx: _Ctx) -> Tensor:
     e = ctx.expr
     out_fmt = ctx.out_fmt
@@ -714,9 +800,15 @@ def _dispatch(ctx: _Ctx) -> Tensor:
         sp = _match_spmm(term, out_vars)
         if sp is not None:
             return _exec_sparse_spmm(ctx, sp)
+        g = _match_spgemm(term, out_vars)
+        if g is not None:
+            return _exec_spgemm(ctx, g)
+    ew = _match_ewise(terms, out_vars)
+    if ew is not None:
+        return _exec_ewise(ctx, *ew)
     raise UnsupportedExpressionError(
         f"no device kernel for {e.output_name} with output format {out_fmt.name()} "
-        "(sparse x sparse, element-wise sparse and multi-term sparse outputs are out of scope)")
+        "(supported sparse outputs: SDDMM, MTTKRP, COO/DCSR/CSC SpMM, CSR SpGEMM, CSR + CSR, CSR .* CSR)")
 
 
 # ---------------------------------------------------------------------------

@@ -16,6 +16,7 @@ import torch
 
 from . import _abi
 from ._abi import check, lib, ptr, require_cuda, stream_handle
+from .tensor import ShapeError
 
 # Items (row ends + stored entries) per sub-warp in the merge-path split; 0 means
 # "plan it": whole waves of resident CTAs (stc_merge_plan_items_per_group).
@@ -437,7 +438,8 @@ def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | N
 def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tensor, *,
                 variant: str = "merge", partition: MergePartition | None = None,
                 workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """``M[s, :] = sum_{p in segment s} (T[p] * B[j[p], :]) * C[k[p], :]`` -> [n_seg, R]."""
+    """``M[s, :] = sum_{p in segment s} T[p] * B[j[p], :] * C[k[p], :]`` -> [n_seg, R]
+    (evaluated per (i,j) fiber: B[j, :] times the fiber's sum of T * C[k, :])."""
     require_cuda(jcrd, kcrd, vals, B, C)
     R = B.shape[1]
     if C.shape[1] != R or B.stride(1) != 1 or C.stride(1) != 1:
@@ -459,3 +461,83 @@ def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tenso
         stream_handle())
     check(rc, "stc_mttkrp_coo3_f32")
     return M
+
+
+# ---------------------------------------------------------------------------
+# Sparse x sparse: SpGEMM and element-wise union / product
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class CsrResult:
+    """A CSR matrix produced on the device (int32 indices, fp32 values)."""
+
+    rowptr: torch.Tensor
+    colidx: torch.Tensor
+    vals: torch.Tensor
+    products: int = 0   # SpGEMM: number of scalar products (the counter law's P)
+
+
+def _byte_buffer(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals) -> CsrResult:
+    """``C(i,k) = A(i,j) * B(j,k)`` for CSR A [m, n], B [n, p] -> CSR C [m, p].
+
+    Every (i,k) reached by a product is stored (arithmetic zeros kept) and each
+    value is summed from 0.0 in ascending j, like the reference's workspace
+    (engine.py:577-644, 71-90). Two host reads size the outputs.
+    """
+    a_rowptr, a_colidx, b_rowptr, b_colidx = map(_i32, (a_rowptr, a_colidx, b_rowptr, b_colidx))
+    a_vals, b_vals = _f32(a_vals), _f32(b_vals)
+    require_cuda(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals)
+    m = a_rowptr.numel() - 1
+    n = b_rowptr.numel() - 1
+    dev = a_rowptr.device
+    L = lib()
+    prod_ptr = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    tmp = _byte_buffer(L.stc_spgemm_products_temp_bytes(m), dev)
+    check(L.stc_spgemm_products(m, ptr(a_rowptr), ptr(a_colidx), ptr(b_rowptr), ptr(prod_ptr), ptr(tmp),
+                                tmp.numel(), stream_handle()), "stc_spgemm_products")
+    products = int(prod_ptr[m].item())
+    ws_bytes = int(L.stc_spgemm_workspace_bytes(m, products))
+    if ws_bytes == 0:
+        raise ShapeError(f"SpGEMM with {products} products exceeds the int32 range of the device path")
+    ws = _byte_buffer(ws_bytes, dev)
+    c_rowptr = torch.empty(m + 1, dtype=torch.int32, device=dev)
+    check(L.stc_spgemm_symbolic(m, n, ptr(a_rowptr), ptr(a_colidx), ptr(a_vals), ptr(b_rowptr), ptr(b_colidx),
+                                ptr(b_vals), ptr(prod_ptr), products, ptr(ws), ws.numel(), ptr(c_rowptr),
+                                stream_handle()), "stc_spgemm_symbolic")
+    nnz = int(c_rowptr[m].item())
+    c_colidx = torch.empty(nnz, dtype=torch.int32, device=dev)
+    c_vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    check(L.stc_spgemm_numeric(m, products, ptr(ws), ws.numel(), ptr(c_rowptr), ptr(c_colidx), ptr(c_vals),
+                               stream_handle()), "stc_spgemm_numeric")
+    return CsrResult(c_rowptr, c_colidx, c_vals, products)
+
+
+def csr_ewise(op: str, a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals) -> CsrResult:
+    """Element-wise CSR of the same shape: ``op="add"`` (union, (0 + a) + b) or
+    ``op="mul"`` (intersection, 0 + a * b), the reference's `_union_sorted` /
+    `_intersect_sorted` co-iteration (engine.py:208-230)."""
+    code = {"add": _abi.EWISE_UNION, "mul": _abi.EWISE_INTERSECT}[op]
+    a_rowptr, a_colidx, b_rowptr, b_colidx = map(_i32, (a_rowptr, a_colidx, b_rowptr, b_colidx))
+    a_vals, b_vals = _f32(a_vals), _f32(b_vals)
+    require_cuda(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals)
+    m = a_rowptr.numel() - 1
+    if b_rowptr.numel() != m + 1:
+        raise ShapeError("element-wise operands need the same number of rows")
+    dev = a_rowptr.device
+    L = lib()
+    c_rowptr = torch.empty(m + 1, dtype=torch.int32, device=dev)
+    tmp = _byte_buffer(L.stc_csr_ewise_temp_bytes(m), dev)
+    check(L.stc_csr_ewise_symbolic(code, m, ptr(a_rowptr), ptr(a_colidx), ptr(b_rowptr), ptr(b_colidx),
+                                   ptr(c_rowptr), ptr(tmp), tmp.numel(), stream_handle()), "stc_csr_ewise_symbolic")
+    nnz = int(c_rowptr[m].item())
+    c_colidx = torch.empty(nnz, dtype=torch.int32, device=dev)
+    c_vals = torch.empty(nnz, dtype=torch.float32, device=dev)
+    check(L.stc_csr_ewise_f32(code, m, ptr(a_rowptr), ptr(a_colidx), ptr(a_vals), ptr(b_rowptr), ptr(b_colidx),
+                              ptr(b_vals), ptr(c_rowptr), ptr(c_colidx), ptr(c_vals), stream_handle()),
+          "stc_csr_ewise_f32")
+    return CsrResult(c_rowptr, c_colidx, c_vals)

@@ -340,9 +340,62 @@ def dense_matmul():
     return run_case("dense_matmul", "C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
 
 
+@case
+def spgemm_csr():
+    # sparse x sparse: CSR out, workspace over k, empty rows on both sides
+    rng = np.random.default_rng(119)
+    A = st.build_from_entries((23, 17), st.csr(23, 17), rand_sparse_entries(rng, (23, 17), 0.2, 0.05, (2, 11)), "A")
+    B = st.build_from_entries((17, 19), st.csr(17, 19), rand_sparse_entries(rng, (17, 19), 0.25, 0.0, (4,)), "B")
+    return run_case("spgemm_csr", "C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
+
+
+@case
+def spgemm_csr_skewed():
+    # one dense row of A and one dense row of B: long product runs per output coordinate
+    rng = np.random.default_rng(120)
+    n = 40
+    ents_a = rand_sparse_entries(rng, (n, n), 0.05)
+    ents_a = [e for e in ents_a if e[0][0] != 5] + [((5, j), float(f32(rng.uniform(-1, 1)))) for j in range(n)]
+    ents_b = rand_sparse_entries(rng, (n, n), 0.08)
+    ents_b = [e for e in ents_b if e[0][0] != 9] + [((9, k), float(f32(rng.uniform(-1, 1)))) for k in range(n)]
+    A = st.build_from_entries((n, n), st.csr(n, n), ents_a, "A")
+    B = st.build_from_entries((n, n), st.csr(n, n), ents_b, "B")
+    return run_case("spgemm_csr_skewed", "C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
+
+
+@case
+def kat_spgemm_zero_kept():
+    # products that cancel still store their coordinate (tests/test_engine.py:186-192 semantics)
+    A = st.build_from_entries((2, 2), st.csr(2, 2), [((0, 0), 1.0), ((0, 1), 1.0), ((1, 1), 2.0)], name="A")
+    B = st.build_from_entries((2, 2), st.csr(2, 2), [((0, 0), 3.0), ((1, 0), -3.0), ((1, 1), 0.5)], name="B")
+    return run_case("kat_spgemm_zero_kept", "C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
+
+
+@case
+def ewise_add_csr():
+    rng = np.random.default_rng(121)
+    A = st.build_from_entries((21, 26), st.csr(21, 26), rand_sparse_entries(rng, (21, 26), 0.2, 0.05, (3,)), "A")
+    B = st.build_from_entries((21, 26), st.csr(21, 26), rand_sparse_entries(rng, (21, 26), 0.3, 0.0, (3, 8)), "B")
+    return run_case("ewise_add_csr", "C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B})
+
+
+@case
+def ewise_mul_csr():
+    rng = np.random.default_rng(122)
+    A = st.build_from_entries((21, 26), st.csr(21, 26), rand_sparse_entries(rng, (21, 26), 0.35, 0.05, (6,)), "A")
+    B = st.build_from_entries((21, 26), st.csr(21, 26), rand_sparse_entries(rng, (21, 26), 0.3, 0.0, (8,)), "B")
+    return run_case("ewise_mul_csr", "C(i,j) = A(i,j) * B(i,j)", {"A": A, "B": B})
+
+
 def main():
+    only = set(sys.argv[1:])
     index = {}
+    idx_path = OUT / "index.json"
+    if only and idx_path.exists():
+        index = json.loads(idx_path.read_text())
     for name, fn in CASES.items():
+        if only and name not in only:
+            continue
         index[name] = fn()
         print(f"{name}: {index[name]['out_format']} counters={index[name]['counters']}")
     (OUT / "index.json").write_text(json.dumps(index, indent=1, sort_keys=True))

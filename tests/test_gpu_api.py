@@ -89,10 +89,14 @@ def test_unsupported_raises_no_fallback():
 
     A = random_tensor(r, (6, 6), "csr", 0.3, "A")
     B = random_tensor(r, (6, 6), "csr", 0.3, "B")
-    with pytest.raises(st.UnsupportedExpressionError):
-        st.run(st.parse("C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B}))  # SpGEMM: out of scope
-    with pytest.raises(st.UnsupportedExpressionError):
-        st.run(st.parse("C(i,j) = A(i,j) + B(i,j)", {"A": A, "B": B}))
+    D = random_tensor(r, (6, 6), "csr", 0.3, "D")
+    Ad = random_tensor(r, (6, 6), "dcsr", 0.3, "Ad")
+    with pytest.raises(st.UnsupportedExpressionError):  # three sparse factors
+        st.run(st.parse("C(i,j) = A(i,j) * B(i,j) * D(i,j)", {"A": A, "B": B, "D": D}))
+    with pytest.raises(st.UnsupportedExpressionError):  # three sparse terms
+        st.run(st.parse("C(i,j) = A(i,j) + B(i,j) + D(i,j)", {"A": A, "B": B, "D": D}))
+    with pytest.raises(st.UnsupportedExpressionError):  # SpGEMM needs CSR operands
+        st.run(st.parse("C(i,k) = Ad(i,j) * B(j,k)", {"Ad": Ad, "B": B}))
     Bd = st.from_dense(r.uniform(-1, 1, (6, 4)), name="Bd")
     with pytest.raises(st.UnsupportedExpressionError):
         st.run(st.parse("C(i,k) = A(i,j) * Bd(j,k)", {"A": A, "Bd": Bd}), out_format=st.csr(6, 4))

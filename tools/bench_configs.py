@@ -21,7 +21,7 @@ import torch
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-from oracle import native  # noqa: E402
+from oracle import native, restate  # noqa: E402
 from paper_2405_16883_b200 import ops, synthetic  # noqa: E402
 
 torch.backends.cuda.matmul.allow_tf32 = False
@@ -194,13 +194,43 @@ def cfg5():
                   {"nnz": nnz, "items_per_group": part.items_per_group, "row0_nnz": int(ptr[1])})
 
 
+def spgemm_cfg1():
+    """§8(f)-3: SpGEMM A @ A on the cfg1 matrix (CSR x CSR -> CSR, expand-sort-compress)."""
+    A, _ = synthetic.cfg1()
+    R, C, V = dev_csr(A)
+    res = ops.spgemm_csr(R, C, V, R, C, V)
+    P = res.products
+    nnz_c = res.vals.numel()
+    ms = gpu_time(lambda: ops.spgemm_csr(R, C, V, R, C, V))
+    flops = 2.0 * P
+    nbytes = 2 * (4 * (A.shape[0] + 1) + 8 * A.nnz) + 4 * (A.shape[0] + 1) + 8 * nnz_c
+    cs = cpu_time(lambda: restate.spgemm_csr(A.rowptr, A.colidx, A.vals, A.rowptr, A.colidx, A.vals), 3.0)
+    return record("x1_spgemm_cfg1_AxA", ms, flops, nbytes, "hbm", cs, "numpy restatement (1 thread)",
+                  {"products": P, "nnz_out": nnz_c, "cpu_threads_note": "numpy, single thread"})
+
+
+def ewise_cfg1():
+    """§8(f)-3: element-wise union A + B of two independent cfg1 draws (167k entries each)."""
+    A, _ = synthetic.cfg1()
+    B, _ = synthetic.cfg1(base=1)  # an independent draw of the same recipe (~1 % overlap)
+    R, C, V = dev_csr(A)
+    R2, C2, V2 = dev_csr(B)
+    res = ops.csr_ewise("add", R, C, V, R2, C2, V2)
+    ms = gpu_time(lambda: ops.csr_ewise("add", R, C, V, R2, C2, V2))
+    nnz_c = res.vals.numel()
+    nbytes = 2 * (4 * (A.shape[0] + 1)) + 8 * (A.nnz + B.nnz) + 4 * (A.shape[0] + 1) + 8 * nnz_c
+    cs = cpu_time(lambda: restate.csr_ewise("add", A.rowptr, A.colidx, A.vals, B.rowptr, B.colidx, B.vals), 3.0)
+    return record("x2_csr_add_cfg1", ms, float(nnz_c), nbytes, "hbm", cs, "numpy restatement (1 thread)",
+                  {"nnz_out": nnz_c})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--configs", default="1,2,3,4,5,x1,x2")
     a = ap.parse_args()
-    fns = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
-    res = [fns[int(c)]() for c in a.configs.split(",")]
+    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "x1": spgemm_cfg1, "x2": ewise_cfg1}
+    res = [fns[c]() for c in a.configs.split(",")]
     if a.out:
         Path(a.out).write_text(json.dumps({"device": PROPS.name, "sms": PROPS.multi_processor_count,
                                            "results": res}, indent=1))
