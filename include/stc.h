@@ -194,19 +194,23 @@ int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd
  * Three phases, sizes read back by the caller between them:
  *   1. stc_spgemm_products: prod_ptr[m+1] = exclusive scan of per-row product
  *      counts; products = prod_ptr[m] (temp: stc_spgemm_products_temp_bytes).
- *   2. stc_spgemm_symbolic: expands and sorts the products into `ws`
- *      (stc_spgemm_workspace_bytes(m, products)) and writes c_rowptr[m+1].
- *   3. stc_spgemm_numeric: c_colidx / c_vals (c_rowptr[m] entries) from `ws`. */
+ *   2. stc_spgemm_symbolic: writes c_rowptr[m+1] (workspace `ws` of
+ *      stc_spgemm_workspace_bytes(m, p, products) bytes; p = columns of B).
+ *   3. stc_spgemm_numeric: c_colidx / c_vals (c_rowptr[m] entries).
+ * B with p <= 6144 columns: a per-warp SMEM accumulator over the whole output
+ * row; wider B: expand, stable segmented sort, compress (products < 2^31).   */
 size_t stc_spgemm_products_temp_bytes(int m);
 int stc_spgemm_products(int m, const int* a_rowptr, const int* a_colidx, const int* b_rowptr,
                         long long* prod_ptr, void* temp, size_t temp_bytes, void* stream);
-size_t stc_spgemm_workspace_bytes(int m, long long products);
-int stc_spgemm_symbolic(int m, int n, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+size_t stc_spgemm_workspace_bytes(int m, int p, long long products);
+int stc_spgemm_symbolic(int m, int p, const int* a_rowptr, const int* a_colidx, const float* a_vals,
                         const int* b_rowptr, const int* b_colidx, const float* b_vals,
                         const long long* prod_ptr, long long products, void* ws, size_t ws_bytes,
                         int* c_rowptr, void* stream);
-int stc_spgemm_numeric(int m, long long products, void* ws, size_t ws_bytes, const int* c_rowptr,
-                       int* c_colidx, float* c_vals, void* stream);
+int stc_spgemm_numeric(int m, int p, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+                       const int* b_rowptr, const int* b_colidx, const float* b_vals, long long products,
+                       void* ws, size_t ws_bytes, const int* c_rowptr, int* c_colidx, float* c_vals,
+                       void* stream);
 
 /* Element-wise CSR (same shape): STC_EWISE_UNION C = A + B (two terms, the
  * reference's _union_sorted, engine.py:224-230; value (0 + a) + b, or 0 + a /

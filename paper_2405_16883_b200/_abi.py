@@ -75,9 +75,9 @@ SIGNATURES = {
                                  _p, _sz, _p]),
     "stc_spgemm_products_temp_bytes": (_sz, [_i]),
     "stc_spgemm_products": (_i, [_i, _p, _p, _p, _p, _p, _sz, _p]),
-    "stc_spgemm_workspace_bytes": (_sz, [_i, _ll]),
+    "stc_spgemm_workspace_bytes": (_sz, [_i, _i, _ll]),
     "stc_spgemm_symbolic": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _p, _ll, _p, _sz, _p, _p]),
-    "stc_spgemm_numeric": (_i, [_i, _ll, _p, _sz, _p, _p, _p, _p]),
+    "stc_spgemm_numeric": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _ll, _p, _sz, _p, _p, _p, _p]),
     "stc_csr_ewise_temp_bytes": (_sz, [_i]),
     "stc_csr_ewise_symbolic": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "stc_csr_ewise_f32": (_i, [_i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),

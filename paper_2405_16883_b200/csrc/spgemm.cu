@@ -13,10 +13,12 @@
 // a_ij * b_jk), term order for the union ((0 + a) + b), and 0 + a * b for the
 // product — evaluated in fp32.
 //
-// SpGEMM is expand-sort-compress, row by row: a warp per row writes the row's
-// products (key k, value a*b) in (j, k) order; a stable segmented sort by k
-// (CUB) keeps equal keys in ascending j; a warp per row then sums each run
-// left to right. Union / product: a warp per row, each lane binary-searches its
+// SpGEMM, B with at most kDenseMaxCols columns: a warp per row accumulates into
+// a private SMEM window over all output columns (values + touched bitmask),
+// walking j in ascending order — no sort, no product buffer. Wider B:
+// expand-sort-compress, row by row: a warp per row writes the row's products
+// (key k, value a*b) in (j, k) order; a stable segmented sort by k (CUB) keeps
+// equal keys in ascending j; a warp per row then sums each run left to right. Union / product: a warp per row, each lane binary-searches its
 // entries in the other operand's row; ballots give output ranks, so rows of any
 // length spread over 32 lanes.
 #include <cub/device/device_scan.cuh>
@@ -118,6 +120,92 @@ __global__ void spgemm_compress_kernel(int m, const int* __restrict__ seg, const
       cv[o] = acc;
     }
     out += __popc(ball);
+  }
+}
+
+// ---- dense-window SpGEMM (B has at most kDenseMaxCols columns) ----------------------------
+//
+// A warp owns one row at a time and a private SMEM accumulator over all p output
+// columns (fp32 values + a touched bitmask). It walks A's row in ascending j;
+// for each j the lanes scatter B_j's entries (distinct k, so no conflicts):
+// acc[k] = acc[k] + a*b, bit k set. __syncwarp between j steps keeps every
+// acc[k] summed in ascending j from 0.0, deterministically. Phase 0 counts the
+// set bits of the row; phase 1 emits (k, acc[k]) in ascending k by a ballot /
+// popc scan over the bitmask words and clears what it read.
+constexpr int kDenseMaxCols = 6144;
+
+__host__ __device__ inline int dense_words(int p) { return (p + 31) / 32; }
+__host__ __device__ inline size_t dense_warp_bytes(int p) {
+  return (size_t)dense_words(p) * 4 + (size_t)((p + 31) / 32 * 32) * 4;
+}
+inline int dense_warps_per_cta(int p) {
+  const size_t per = dense_warp_bytes(p);
+  int w = (int)((200u * 1024u) / per);
+  return w > 8 ? 8 : w;
+}
+
+__global__ void spgemm_dense_kernel(int phase, int m, int p, const int* __restrict__ ap, const int* __restrict__ aj,
+                                    const float* __restrict__ av, const int* __restrict__ bp,
+                                    const int* __restrict__ bj, const float* __restrict__ bv,
+                                    int* __restrict__ cnt, const int* __restrict__ cp, int* __restrict__ ck,
+                                    float* __restrict__ cv) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int nw = blockDim.x / 32, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int words = dense_words(p);
+  const int pad = words * 32;
+  unsigned* bits = reinterpret_cast<unsigned*>(dsm) + warp * words;
+  float* acc = reinterpret_cast<float*>(dsm + (size_t)nw * words * 4) + (size_t)warp * pad;
+  for (int w = lane; w < words; w += 32) bits[w] = 0u;
+  if (phase == 1)
+    for (int k = lane; k < pad; k += 32) acc[k] = 0.0f;
+  __syncwarp();
+  for (int row = blockIdx.x * nw + warp; row < m; row += gridDim.x * nw) {
+    for (int q = ap[row]; q < ap[row + 1]; ++q) {
+      const int j = aj[q];
+      const float a = av[q];
+      for (int t = bp[j] + lane; t < bp[j + 1]; t += 32) {
+        const int k = bj[t];
+        atomicOr(&bits[k >> 5], 1u << (k & 31));
+        if (phase == 1) acc[k] += a * bv[t];
+      }
+      __syncwarp();
+    }
+    if (phase == 0) {
+      int c = 0;
+      for (int w = lane; w < words; w += 32) {
+        c += __popc(bits[w]);
+        bits[w] = 0u;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) cnt[row] = c;
+    } else {
+      int out = cp[row];
+      for (int base = 0; base < words; base += 32) {
+        const int w = base + lane;
+        unsigned b = w < words ? bits[w] : 0u;
+        const int c = __popc(b);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int o = out + incl - c;
+        while (b) {
+          const int bit = __ffs(b) - 1;
+          b &= b - 1;
+          const int k = w * 32 + bit;
+          ck[o] = k;
+          cv[o] = acc[k];
+          acc[k] = 0.0f;
+          ++o;
+        }
+        if (w < words) bits[w] = 0u;
+        out += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -288,21 +376,75 @@ extern "C" int stc_spgemm_products(int m, const int* a_rowptr, const int* a_coli
   return check_launch("spgemm_products");
 }
 
-extern "C" size_t stc_spgemm_workspace_bytes(int m, long long products) {
-  if (m < 0 || products < 0 || products > INT32_MAX) return 0;
+namespace {
+bool use_dense(int p) { return p <= kDenseMaxCols; }
+
+struct DenseLaunch {
+  int warps;
+  size_t smem;
+  unsigned grid;
+};
+DenseLaunch dense_launch(int m, int p) {
+  DenseLaunch d;
+  const size_t per = dense_warp_bytes(p);
+  int w = (int)((72u * 1024u) / per);
+  d.warps = w < 1 ? 1 : (w > 8 ? 8 : w);
+  d.smem = per * d.warps;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spgemm_dense_kernel, d.warps * 32, d.smem);
+  const long long want = ceil_div(m, d.warps);
+  const long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  d.grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+  return d;
+}
+int launch_dense(int phase, int m, int p, const int* ap, const int* aj, const float* av, const int* bp,
+                 const int* bj, const float* bv, int* cnt, const int* cp, int* ck, float* cv, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(spgemm_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  if (m == 0) return STC_OK;
+  const DenseLaunch d = dense_launch(m, p);
+  spgemm_dense_kernel<<<d.grid, d.warps * 32, d.smem, st>>>(phase, m, p, ap, aj, av, bp, bj, bv, cnt, cp, ck, cv);
+  return check_launch("spgemm_dense_kernel");
+}
+size_t dense_ws_bytes(int m) { return align256(((size_t)m + 1) * 4) + scan_int_bytes(m + 1) + 256; }
+}  // namespace
+
+extern "C" size_t stc_spgemm_workspace_bytes(int m, int p, long long products) {
+  if (m < 0 || p < 0 || products < 0) return 0;
+  if (use_dense(p)) return dense_ws_bytes(m);
+  if (products > INT32_MAX) return 0;
   return spgemm_ws_layout(m, products, nullptr, nullptr);
 }
 
-extern "C" int stc_spgemm_symbolic(int m, int n, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+extern "C" int stc_spgemm_symbolic(int m, int p, const int* a_rowptr, const int* a_colidx, const float* a_vals,
                                    const int* b_rowptr, const int* b_colidx, const float* b_vals,
                                    const long long* prod_ptr, long long products, void* ws, size_t ws_bytes,
                                    int* c_rowptr, void* stream) {
-  if (m < 0 || n < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
-  if (products > INT32_MAX) return fail(STC_EUNSUPPORTED, "%lld products exceed the int32 range", products);
+  if (m < 0 || p < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
   if (!a_rowptr || !b_rowptr || !prod_ptr || !c_rowptr || !ws) return fail(STC_EINVAL, "null pointer");
-  const size_t need = stc_spgemm_workspace_bytes(m, products);
+  const size_t need = stc_spgemm_workspace_bytes(m, p, products);
+  if (need == 0) return fail(STC_EUNSUPPORTED, "%lld products exceed the int32 range", products);
   if (ws_bytes < need) return fail(STC_EWORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_dense(p)) {
+    char* b = static_cast<char*>(align_base(ws));
+    int* cnt = reinterpret_cast<int*>(b);
+    void* tmp = b + align256(((size_t)m + 1) * 4);
+    cudaMemsetAsync(cnt + m, 0, sizeof(int), st);
+    if (int rc = launch_dense(0, m, p, a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals, cnt, nullptr,
+                              nullptr, nullptr, st))
+      return rc;
+    size_t tb = scan_int_bytes(m + 1);
+    const cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, c_rowptr, m + 1, st);
+    if (e != cudaSuccess) return fail(STC_ELAUNCH, "spgemm row scan: %s", cudaGetErrorString(e));
+    return check_launch("spgemm_symbolic");
+  }
   SpgemmWs w;
   spgemm_ws_layout(m, products, align_base(ws), &w);
   spgemm_expand_kernel<<<grid_rows(m + 1), kWarpsPerCta * 32, 0, st>>>(
@@ -322,15 +464,21 @@ extern "C" int stc_spgemm_symbolic(int m, int n, const int* a_rowptr, const int*
   return check_launch("spgemm_symbolic");
 }
 
-extern "C" int stc_spgemm_numeric(int m, long long products, void* ws, size_t ws_bytes, const int* c_rowptr,
-                                  int* c_colidx, float* c_vals, void* stream) {
-  if (m < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
+extern "C" int stc_spgemm_numeric(int m, int p, const int* a_rowptr, const int* a_colidx, const float* a_vals,
+                                  const int* b_rowptr, const int* b_colidx, const float* b_vals, long long products,
+                                  void* ws, size_t ws_bytes, const int* c_rowptr, int* c_colidx, float* c_vals,
+                                  void* stream) {
+  if (m < 0 || p < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
   if (!ws || !c_rowptr) return fail(STC_EINVAL, "null pointer");
-  const size_t need = stc_spgemm_workspace_bytes(m, products);
+  const size_t need = stc_spgemm_workspace_bytes(m, p, products);
+  if (need == 0) return fail(STC_EUNSUPPORTED, "%lld products exceed the int32 range", products);
   if (ws_bytes < need) return fail(STC_EWORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_dense(p))
+    return launch_dense(1, m, p, a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals, nullptr, c_rowptr,
+                        c_colidx, c_vals, st);
   SpgemmWs w;
   spgemm_ws_layout(m, products, align_base(ws), &w);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   spgemm_compress_kernel<<<grid_rows(m), kWarpsPerCta * 32, 0, st>>>(m, w.seg, w.keys_out, w.vals_out, c_rowptr,
                                                                      c_colidx, c_vals);
   return check_launch("spgemm_compress_kernel");

@@ -739,8 +739,8 @@ def _exec_spgemm(ctx: _Ctx, g: _SpgemmTerm) -> Tensor:
     if not (_is_csr(A) and _is_csr(B)):
         raise UnsupportedExpressionError("device SpGEMM needs CSR operands accessed in storage order")
     la, lb = A.storage.levels[1], B.storage.levels[1]
-    r = ops.spgemm_csr(la.pos, la.crd, A.storage.values, lb.pos, lb.crd, B.storage.values)
-    ctx.chosen.append("spgemm:esc")
+    r = ops.spgemm_csr(la.pos, la.crd, A.storage.values, lb.pos, lb.crd, B.storage.values, B.shape[1])
+    ctx.chosen.append("spgemm:dense-window" if B.shape[1] <= 6144 else "spgemm:esc")
     m, nnz_a = A.shape[0], int(A.storage.values.numel())
     ctx.counter.add(r.products, r.products, m + 2 * nnz_a + 2 * r.products)
     return _csr_out(ctx, (A.shape[0], B.shape[1]), r)

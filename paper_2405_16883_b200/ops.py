@@ -482,8 +482,8 @@ def _byte_buffer(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
-def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals) -> CsrResult:
-    """``C(i,k) = A(i,j) * B(j,k)`` for CSR A [m, n], B [n, p] -> CSR C [m, p].
+def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals, n_cols: int) -> CsrResult:
+    """``C(i,k) = A(i,j) * B(j,k)`` for CSR A [m, n], B [n, n_cols] -> CSR C [m, n_cols].
 
     Every (i,k) reached by a product is stored (arithmetic zeros kept) and each
     value is summed from 0.0 in ascending j, like the reference's workspace
@@ -493,27 +493,27 @@ def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals) -> CsrRes
     a_vals, b_vals = _f32(a_vals), _f32(b_vals)
     require_cuda(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals)
     m = a_rowptr.numel() - 1
-    n = b_rowptr.numel() - 1
     dev = a_rowptr.device
     L = lib()
+    A = (ptr(a_rowptr), ptr(a_colidx), ptr(a_vals))
+    B = (ptr(b_rowptr), ptr(b_colidx), ptr(b_vals))
     prod_ptr = torch.empty(m + 1, dtype=torch.int64, device=dev)
     tmp = _byte_buffer(L.stc_spgemm_products_temp_bytes(m), dev)
-    check(L.stc_spgemm_products(m, ptr(a_rowptr), ptr(a_colidx), ptr(b_rowptr), ptr(prod_ptr), ptr(tmp),
-                                tmp.numel(), stream_handle()), "stc_spgemm_products")
+    check(L.stc_spgemm_products(m, A[0], A[1], B[0], ptr(prod_ptr), ptr(tmp), tmp.numel(), stream_handle()),
+          "stc_spgemm_products")
     products = int(prod_ptr[m].item())
-    ws_bytes = int(L.stc_spgemm_workspace_bytes(m, products))
+    ws_bytes = int(L.stc_spgemm_workspace_bytes(m, n_cols, products))
     if ws_bytes == 0:
         raise ShapeError(f"SpGEMM with {products} products exceeds the int32 range of the device path")
     ws = _byte_buffer(ws_bytes, dev)
     c_rowptr = torch.empty(m + 1, dtype=torch.int32, device=dev)
-    check(L.stc_spgemm_symbolic(m, n, ptr(a_rowptr), ptr(a_colidx), ptr(a_vals), ptr(b_rowptr), ptr(b_colidx),
-                                ptr(b_vals), ptr(prod_ptr), products, ptr(ws), ws.numel(), ptr(c_rowptr),
+    check(L.stc_spgemm_symbolic(m, n_cols, *A, *B, ptr(prod_ptr), products, ptr(ws), ws.numel(), ptr(c_rowptr),
                                 stream_handle()), "stc_spgemm_symbolic")
     nnz = int(c_rowptr[m].item())
     c_colidx = torch.empty(nnz, dtype=torch.int32, device=dev)
     c_vals = torch.empty(nnz, dtype=torch.float32, device=dev)
-    check(L.stc_spgemm_numeric(m, products, ptr(ws), ws.numel(), ptr(c_rowptr), ptr(c_colidx), ptr(c_vals),
-                               stream_handle()), "stc_spgemm_numeric")
+    check(L.stc_spgemm_numeric(m, n_cols, *A, *B, products, ptr(ws), ws.numel(), ptr(c_rowptr), ptr(c_colidx),
+                               ptr(c_vals), stream_handle()), "stc_spgemm_numeric")
     return CsrResult(c_rowptr, c_colidx, c_vals, products)
 
 

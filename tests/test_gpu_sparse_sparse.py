@@ -64,6 +64,11 @@ SPGEMM = {
     "single": lambda r: ((1, 1, [1]), (1, 1, [1])),
     "power_law": lambda r: ((2000, 2000, np.minimum((2000 / (np.arange(2000) + 1)) ** 0.8 + 1, 2000).astype(int)),
                             (2000, 2000, r.integers(0, 8, 2000))),
+    # B wider than the SMEM window (6144 columns): expand-sort-compress path
+    "wide_esc": lambda r: ((120, 300, r.integers(0, 25, 120)), (300, 20000, r.integers(0, 40, 300))),
+    "wide_esc_dense_row": lambda r: ((30, 100, np.where(np.arange(30) == 3, 100, r.integers(0, 4, 30))),
+                                     (100, 9000, np.where(np.arange(100) == 10, 9000, r.integers(0, 30, 100)))),
+    "wide_esc_no_products": lambda r: ((10, 6, np.full(10, 2)), (6, 7000, np.zeros(6, dtype=np.int64))),
 }
 
 
@@ -75,7 +80,7 @@ def test_spgemm(struct):
     A = make_csr(rng, m, n, la, zero_frac=0.05)
     B = make_csr(rng, n, p, lb)
     want = restate.spgemm_csr(*A, *B)
-    res = ops.spgemm_csr(*dev(*A), *dev(*B))
+    res = ops.spgemm_csr(*dev(*A), *dev(*B), p)
     assert res.products == int(np.diff(B[0])[A[1]].sum())
     bound = dense_of(*A, (m, n)).__abs__() @ dense_of(*B, (n, p)).__abs__()
     check(res, want, bound, (m, p))
@@ -85,7 +90,7 @@ def test_spgemm_deterministic():
     rng = np.random.default_rng(5)
     A = dev(*make_csr(rng, 500, 400, rng.integers(0, 20, 500)))
     B = dev(*make_csr(rng, 400, 300, rng.integers(0, 20, 400)))
-    r1, r2 = ops.spgemm_csr(*A, *B), ops.spgemm_csr(*A, *B)
+    r1, r2 = ops.spgemm_csr(*A, *B, 300), ops.spgemm_csr(*A, *B, 300)
     assert torch.equal(r1.colidx, r2.colidx) and torch.equal(r1.vals, r2.vals)
 
 
@@ -113,7 +118,7 @@ def test_csr_ewise(struct, op):
 
 def test_ewise_values_follow_reference_order():
     # (0 + a) + b: a lone -0.0 becomes +0.0 in the workspace, like the reference's dict slot
-    rp = np.array([0, 2]); A = (rp, np.array([0, 1]), np.array([-0.0, 1.5], dtype=np.float32))
+    A = (np.array([0, 2]), np.array([0, 1]), np.array([-0.0, 1.5], dtype=np.float32))
     B = (np.array([0, 1]), np.array([1]), np.array([2.25], dtype=np.float32))
     res = ops.csr_ewise("add", *dev(*A), *dev(*B))
     v = res.vals.cpu().numpy()

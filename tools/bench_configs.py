@@ -198,10 +198,10 @@ def spgemm_cfg1():
     """§8(f)-3: SpGEMM A @ A on the cfg1 matrix (CSR x CSR -> CSR, expand-sort-compress)."""
     A, _ = synthetic.cfg1()
     R, C, V = dev_csr(A)
-    res = ops.spgemm_csr(R, C, V, R, C, V)
+    res = ops.spgemm_csr(R, C, V, R, C, V, A.shape[1])
     P = res.products
     nnz_c = res.vals.numel()
-    ms = gpu_time(lambda: ops.spgemm_csr(R, C, V, R, C, V))
+    ms = gpu_time(lambda: ops.spgemm_csr(R, C, V, R, C, V, A.shape[1]))
     flops = 2.0 * P
     nbytes = 2 * (4 * (A.shape[0] + 1) + 8 * A.nnz) + 4 * (A.shape[0] + 1) + 8 * nnz_c
     cs = cpu_time(lambda: restate.spgemm_csr(A.rowptr, A.colidx, A.vals, A.rowptr, A.colidx, A.vals), 3.0)
