@@ -150,11 +150,11 @@ extern "C" int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, in
   t.ml = reinterpret_cast<float2*>(t.Opart + (size_t)heads * m * AT_D);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT_SMEM);
+    cudaFuncSetAttribute(attn_tile8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT8_SMEM);
     configured = true;
   }
-  attn_tile_kernel<<<dim3(n_blocks, heads), AT_THREADS, AT_SMEM, st>>>(t);
-  rc = check_launch("attn_tile_kernel");
+  attn_tile8_kernel<<<dim3(n_blocks, heads), AT8_THREADS, AT8_SMEM, st>>>(t);
+  rc = check_launch("attn_tile8_kernel");
   if (rc) return rc;
   AttnArgs a{};
   a.m = m; a.n = n; a.d = d; a.heads = heads;

@@ -5,11 +5,11 @@
 // are "dense tiles": their mask values are stored as a 64x64 float tile
 // (NaN = absent). Everything else stays a CSR "remainder".
 //
-// attn_tile_kernel: one CTA per (row block, head). Q of the block is staged in
+// attn_tile8_kernel: one CTA per (row block, head). Q of the block is staged in
 // SMEM once; for every dense tile, K and V of its 64 columns are staged and
-//   S = scale * M .* (Q K^T)   (4x4 register tile per thread, LDS.128 operands)
-//   online softmax per row    (row max / sum over the 16 threads of a row)
-//   O += P V                  (4x4 register tile per thread)
+//   S = scale * M .* (Q K^T)   (8x8 register tile per thread, LDS.128 operands)
+//   online softmax per row    (row max / sum over the 8 threads of a row)
+//   O += P V                  (8x8 register tile per thread)
 // run on CUDA cores: each staged K/V row is reused by all 64 rows of the block
 // instead of being gathered once per stored entry. The unnormalised (O, max,
 // sum) of each row is written out; the per-row kernel then folds in the
@@ -22,8 +22,6 @@ namespace stc {
 
 constexpr int AT_B = 64;          // rows per block, columns per tile
 constexpr int AT_D = 64;          // head dim of the tiled path
-constexpr int AT_THREADS = 256;
-constexpr size_t AT_SMEM = 4ull * AT_B * AT_B * sizeof(float);  // Qt, Kt, V, Pt
 
 struct TileArgs {
   int m, n, heads, n_blocks, dt_max;
@@ -40,135 +38,164 @@ struct TileArgs {
   float2* ml;               // [H][M] (running max, running sum)
 };
 
-__global__ void __launch_bounds__(AT_THREADS, 3) attn_tile_kernel(TileArgs a) {
-  extern __shared__ __align__(16) float sm[];
-  float* Qt = sm;                    // [d][row]
-  float* Kt = Qt + AT_B * AT_B;      // [d][col]
-  float* Vs = Kt + AT_B * AT_B;      // [col][d]
-  float* Pt = Vs + AT_B * AT_B;      // [col][row]
+// ---------------------------------------------------------------------------
+// attn_tile8_kernel (64 threads).
+//
+// Thread (ty, tx) = (tid / 8, tid % 8) owns rows {4ty..4ty+3, 32+4ty..32+4ty+3} and
+// columns / head dims {4tx..4tx+3, 32+4tx..32+4tx+3}: per 4-wide slice of the
+// reduction it issues 16 LDS.128 for 256 FMAs (a 4x4 tiling of 256 threads: 8 for
+// 64, and SMEM-wavefront bound at 40 % FMA-pipe use — measured, cfg4 0.85 ms). Q, K and V are staged by
+// cp.async (K and V of tile t+1 once tile t is done; P^T reuses K's buffer so that
+// four CTAs fit an SM and cover each other's copies). K rows are stored with
+// their 16-byte chunks XOR-swizzled by (row / 4) % 8 and P^T with its row chunks
+// swizzled the same way, so the 8 lanes of a quarter-warp hit 8 bank groups.
+// ---------------------------------------------------------------------------
+constexpr int AT8_THREADS = 64;
+constexpr size_t AT8_SMEM = 3ull * AT_B * AT_B * sizeof(float);  // Qs, Ks (aliased by Pt), Vs
+
+STC_DEVICE int at8_row(int ty, int i) { return i < 4 ? 4 * ty + i : 32 + 4 * ty + (i - 4); }
+
+__global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) {
+  extern __shared__ __align__(16) float sm8[];
+  float* Qs = sm8;                  // [row][d]
+  float* Ks = Qs + AT_B * AT_B;     // [col][d], chunk-swizzled
+  float* Vs = Ks + AT_B * AT_B;     // [col][d]
+  float* Pt = Ks;                   // [col][row], row-chunk swizzled (K is dead once S is done)
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;  // rows 4ty..4ty+3, cols / d 4tx..4tx+3
+  const int tx = tid % 8, ty = tid / 8;
   const int row0 = b * AT_B;
   const float* Qh = a.Q + h * a.q_hs;
   const float* Kh = a.K + h * a.k_hs;
   const float* Vh = a.V + h * a.v_hs;
+  const int* cols = a.tile_cols + (long long)b * a.dt_max;
 
-  // lanes walk rows (consecutive r) for a fixed d-quad, so the transposed
-  // scalar stores hit 32 distinct banks
-  for (int idx = tid; idx < AT_B * (AT_D / 4); idx += AT_THREADS) {
-    const int r = idx % AT_B, dq = (idx / AT_B) * 4;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row0 + r < a.m) q = *reinterpret_cast<const float4*>(Qh + (long long)(row0 + r) * a.q_rs + dq);
-    Qt[(dq + 0) * AT_B + r] = q.x;
-    Qt[(dq + 1) * AT_B + r] = q.y;
-    Qt[(dq + 2) * AT_B + r] = q.z;
-    Qt[(dq + 3) * AT_B + r] = q.w;
+  auto stage_rows = [&](float* dst, const float* src, long long rs, int r0, int limit, bool swz) {
+    for (int idx = tid; idx < AT_B * 16; idx += AT8_THREADS) {
+      const int r = idx / 16, dq = idx % 16;
+      const bool ok = r0 + r < limit;
+      const int slot = swz ? (dq ^ ((r >> 2) & 7)) : dq;
+      cp_async16(dst + r * AT_D + slot * 4, ok ? (const void*)(src + (long long)(r0 + r) * rs + dq * 4) : (const void*)src,
+                 ok);
+    }
+    cp_async_commit();
+  };
+  int n_t = 0;
+  while (n_t < a.dt_max && cols[n_t] >= 0) ++n_t;
+  stage_rows(Qs, Qh, a.q_rs, row0, a.m, false);
+  if (n_t > 0) {
+    stage_rows(Ks, Kh, a.k_rs, cols[0] * AT_B, a.n, true);
+    stage_rows(Vs, Vh, a.v_rs, cols[0] * AT_B, a.n, false);
   }
 
-  float o[4][4], mrow[4], lrow[4];
+  float o[8][8], mrow[8], lrow[8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     mrow[i] = -INFINITY;
     lrow[i] = 0.f;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[i][e] = 0.f;
+    for (int e = 0; e < 8; ++e) o[i][e] = 0.f;
   }
-  const unsigned hmask = 0xffffffffu;  // all lanes shuffle; width 16 keeps each row group apart
 
-  for (int t = 0; t < a.dt_max; ++t) {
-    const int tc = a.tile_cols[b * a.dt_max + t];
-    if (tc < 0) break;
-    __syncthreads();  // previous tile's operands fully consumed
-    const int c0 = tc * AT_B;
-    for (int idx = tid; idx < AT_B * (AT_D / 4); idx += AT_THREADS) {
-      const int c = idx % AT_B, dq = (idx / AT_B) * 4;
-      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f), vv = kv;
-      if (c0 + c < a.n) {
-        kv = ld_gather4(Kh + (long long)(c0 + c) * a.k_rs + dq);
-        vv = ld_gather4(Vh + (long long)(c0 + c) * a.v_rs + dq);
-      }
-      Kt[(dq + 0) * AT_B + c] = kv.x;
-      Kt[(dq + 1) * AT_B + c] = kv.y;
-      Kt[(dq + 2) * AT_B + c] = kv.z;
-      Kt[(dq + 3) * AT_B + c] = kv.w;
-      *reinterpret_cast<float4*>(Vs + c * AT_D + dq) = vv;
-    }
+  for (int t = 0; t < n_t; ++t) {
+    cp_async_wait<1>();  // Q and K(t) landed; V(t) may still be in flight
     __syncthreads();
-
-    float s[4][4];
+    float s[8][8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) s[i][j] = 0.f;
-#pragma unroll 8
-    for (int d = 0; d < AT_D; ++d) {
-      const float4 q4 = *reinterpret_cast<const float4*>(Qt + d * AT_B + 4 * ty);
-      const float4 k4 = *reinterpret_cast<const float4*>(Kt + d * AT_B + 4 * tx);
-      const float qa[4] = {q4.x, q4.y, q4.z, q4.w};
-      const float ka[4] = {k4.x, k4.y, k4.z, k4.w};
+      for (int j = 0; j < 8; ++j) s[i][j] = 0.f;
+#pragma unroll 1
+    for (int dq = 0; dq < 16; ++dq) {
+      float4 q4[8], k4[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i) q4[i] = *reinterpret_cast<const float4*>(Qs + at8_row(ty, i) * AT_D + dq * 4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) s[i][j] = fmaf(qa[i], ka[j], s[i][j]);
+      for (int j = 0; j < 8; ++j) {
+        const int c = at8_row(tx, j);
+        k4[j] = *reinterpret_cast<const float4*>(Ks + c * AT_D + ((dq ^ ((c >> 2) & 7)) * 4));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s[i][j] = fmaf(q4[i].x, k4[j].x, s[i][j]);
+          s[i][j] = fmaf(q4[i].y, k4[j].y, s[i][j]);
+          s[i][j] = fmaf(q4[i].z, k4[j].z, s[i][j]);
+          s[i][j] = fmaf(q4[i].w, k4[j].w, s[i][j]);
+        }
     }
+    __syncthreads();  // every warp is done with Ks: P^T takes its place
 
     const float* mv_tile = a.tile_vals + ((long long)(b * a.dt_max + t) * AT_B) * AT_B;
-    float p[4][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 mv4 = ld_stream4(mv_tile + (4 * ty + i) * AT_B + 4 * tx);
-      const float mva[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
+    for (int i = 0; i < 8; ++i) {
+      const int r = at8_row(ty, i);
+      const float4 m0 = ld_stream4(mv_tile + r * AT_B + 4 * tx);
+      const float4 m1 = ld_stream4(mv_tile + r * AT_B + 32 + 4 * tx);
+      const float mva[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
       float tmax = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 8; ++j) {
         s[i][j] = isnan(mva[j]) ? -INFINITY : s[i][j] * mva[j] * a.scale;
         tmax = fmaxf(tmax, s[i][j]);
       }
 #pragma unroll
-      for (int w = 8; w >= 1; w >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(hmask, tmax, w, 16));
+      for (int w = 4; w >= 1; w >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, w));
       const float mnew = fmaxf(mrow[i], tmax);
       const float corr = (mnew == -INFINITY) ? 1.f : expf(mrow[i] - mnew);
       float rsum = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        p[i][j] = (s[i][j] == -INFINITY) ? 0.f : expf(s[i][j] - mnew);
-        rsum += p[i][j];
+      for (int j = 0; j < 8; ++j) {
+        s[i][j] = (s[i][j] == -INFINITY) ? 0.f : expf(s[i][j] - mnew);
+        rsum += s[i][j];
       }
 #pragma unroll
-      for (int w = 8; w >= 1; w >>= 1) rsum += __shfl_xor_sync(hmask, rsum, w, 16);
+      for (int w = 4; w >= 1; w >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, w);
       lrow[i] = lrow[i] * corr + rsum;
       mrow[i] = mnew;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) o[i][e] *= corr;
+      for (int e = 0; e < 8; ++e) o[i][e] *= corr;
     }
-    // P^T in SMEM, float4 slot of rows 4ty.. in column c swizzled to ty ^ ((c >> 2) & 7):
-    // conflict-free stores here and broadcast loads in the PV loop
+    // P^T: column c, row chunk rc (4 rows) stored at chunk rc ^ ((c >> 2) & 7)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = 4 * tx + j;
-      *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * (ty ^ ((c >> 2) & 7))) =
-          make_float4(p[0][j], p[1][j], p[2][j], p[3][j]);
+    for (int j = 0; j < 8; ++j) {
+      const int c = at8_row(tx, j);
+      const int sw = (c >> 2) & 7;
+      *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * (ty ^ sw)) = make_float4(s[0][j], s[1][j], s[2][j], s[3][j]);
+      *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw)) =
+          make_float4(s[4][j], s[5][j], s[6][j], s[7][j]);
     }
+    cp_async_wait<0>();  // V(t) landed
     __syncthreads();
-#pragma unroll 8
+#pragma unroll 2
     for (int c = 0; c < AT_B; ++c) {
-      const float4 p4 = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ ((c >> 2) & 7)));
-      const float4 v4 = *reinterpret_cast<const float4*>(Vs + c * AT_D + 4 * tx);
-      const float pa[4] = {p4.x, p4.y, p4.z, p4.w};
-      const float va[4] = {v4.x, v4.y, v4.z, v4.w};
+      const int sw = (c >> 2) & 7;
+      const float4 pa = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ sw));
+      const float4 pb = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw));
+      const float4 va = *reinterpret_cast<const float4*>(Vs + c * AT_D + 4 * tx);
+      const float4 vb = *reinterpret_cast<const float4*>(Vs + c * AT_D + 32 + 4 * tx);
+      const float p8[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+      const float v8[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) o[i][e] = fmaf(pa[i], va[e], o[i][e]);
+        for (int e = 0; e < 8; ++e) o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
+    }
+    __syncthreads();  // done with Vs and Pt: stream in the next tile's K and V
+    if (t + 1 < n_t) {
+      stage_rows(Ks, Kh, a.k_rs, cols[t + 1] * AT_B, a.n, true);
+      stage_rows(Vs, Vh, a.v_rs, cols[t + 1] * AT_B, a.n, false);
     }
   }
+  cp_async_wait<0>();
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = row0 + 4 * ty + i;
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + at8_row(ty, i);
     if (row >= a.m) continue;
-    *reinterpret_cast<float4*>(a.Opart + ((long long)h * a.m + row) * AT_D + 4 * tx) =
-        make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
+    float* dst = a.Opart + ((long long)h * a.m + row) * AT_D;
+    *reinterpret_cast<float4*>(dst + 4 * tx) = make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
+    *reinterpret_cast<float4*>(dst + 32 + 4 * tx) = make_float4(o[i][4], o[i][5], o[i][6], o[i][7]);
     if (tx == 0) a.ml[(long long)h * a.m + row] = make_float2(mrow[i], lrow[i]);
   }
 }

@@ -53,16 +53,6 @@ __global__ void coltile_plan_kernel(int m, int n_chunks, const int* __restrict__
   }
 }
 
-STC_DEVICE void cp_async16(void* smem, const void* gmem, bool pred) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
-}
-STC_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-STC_DEVICE void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // Per-warp offsets of its CT_RPW rows' entries within one chunk: lane r (< CT_RPW)
 // knows start(r), lane CT_RPW + r knows end(r); returns the exclusive prefix of the

@@ -42,6 +42,18 @@ STC_DEVICE uint64_t policy_evict_last() {
 }
 
 // Gather of a dense-operand vector: read-only (non-coherent) path, L1-cached.
+// cp.async 16-byte copy (L2 -> SMEM, bypassing L1); pred == false zero-fills
+STC_DEVICE void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+STC_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+STC_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 STC_DEVICE float4 ld_gather4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 STC_DEVICE float ld_gather1(const float* p) { return __ldg(p); }
 

@@ -27,7 +27,28 @@ def cfg3():
     return lambda: ops.spmm_csr(R, C, V, Xt, out=out, variant="coltile")
 
 
-fn = {"3": cfg3, "5": cfg5}[sys.argv[1]]()
+def cfg4():
+    M, Q, K, V = synthetic.cfg4()
+    R, C, MV = (torch.from_numpy(M.rowptr).int().cuda(), torch.from_numpy(M.colidx).int().cuda(),
+                torch.from_numpy(M.vals).cuda())
+    Qt, Kt, Vt = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+    plan = ops.attention_tile_plan(R, C, MV, M.shape[1])
+    ws = torch.empty(int(ops.lib().stc_attention_tiled_workspace_bytes(M.shape[0], 16)) // 4, device="cuda")
+    return lambda: ops.sparse_attention_tiled(plan, Qt, Kt, Vt, scale=0.125, workspace=ws)
+
+
+def cfg2():
+    A, X, W1, _ = synthetic.cfg2()
+    R, C, V = (torch.from_numpy(A.rowptr).int().cuda(), torch.from_numpy(A.colidx).int().cuda(),
+               torch.from_numpy(A.vals).cuda())
+    Z = torch.from_numpy(X).cuda() @ torch.from_numpy(W1).cuda()
+    out = torch.empty_like(Z)
+    part = ops.merge_partition(R, A.nnz, k=128)
+    ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", part.items_per_group, 1, "cuda")
+    return lambda: ops.spmm_csr(R, C, V, Z, out=out, relu=True, variant="merge", partition=part, workspace=ws)
+
+
+fn = {"2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5}[sys.argv[1]]()
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
