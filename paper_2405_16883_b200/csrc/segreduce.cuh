@@ -538,9 +538,11 @@ __global__ void __launch_bounds__(256) row_kernel(SegOut o, MergeShape ms, Op op
   acc.zero();
   typename Op::State fst;
   Op::init(fst);
+  typename Op::Item nxt{};
+  if (start + lane < end) nxt = op.load(start + lane, lane == 0);
   for (int base = start; base < end; base += SUBW) {
-    typename Op::Item it{};
-    if (base + lane < end) it = op.load(base + lane, base + lane == start);
+    const typename Op::Item it = nxt;  // the next SUBW entries load while these are gathered
+    if (base + SUBW + lane < end) nxt = op.load(base + SUBW + lane, false);
     const int n = min(SUBW, end - base);
     for (int q0 = 0; q0 < n; q0 += U) {
       typename Op::Pre pre[U];

@@ -49,8 +49,10 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
   const int slabs = (int)ceil_div(o.k, SW);
   if (o.m == 0 || slabs == 0) return STC_OK;
   if (L.variant == STC_VARIANT_ROW) {
+    // a row's sub-warp loads SUBW entries at a time: keep up to 16 of their gathers in flight
+    constexpr int UR = SUBW >= 16 ? 16 : (SUBW >= 8 ? 8 : 4);
     const dim3 grid((unsigned)ceil_div((long long)o.m * SUBW, kThreads), slabs, L.batch);
-    launch_windowed(row_kernel<SUBW, VEC, EPI, ADD, U, Op>, grid, dim3(kThreads), 0, L.stream, L.window,
+    launch_windowed(row_kernel<SUBW, VEC, EPI, ADD, UR, Op>, grid, dim3(kThreads), 0, L.stream, L.window,
                     L.window_bytes, o, ms, op);
     return check_launch("row_kernel");
   }
