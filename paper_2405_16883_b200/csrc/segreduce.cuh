@@ -358,7 +358,21 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
     const int wn = min(CAP, n_nnz - w0);
     __syncwarp(mask);
-    for (int t = lane; t < wn + kStagePad; t += SUBW) items[t] = t < wn ? op.load(s.y + w0 + t, w0 + t == 0) : Op::dummy();
+    // SU loads per lane in flight before their SMEM stores (one latency per SU * SUBW items)
+    constexpr int SU = sizeof(Item) <= 8 ? 8 : 1;
+    for (int t0 = 0; t0 < wn + kStagePad; t0 += SU * SUBW) {
+      Item tmp[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int t = t0 + u * SUBW + lane;
+        tmp[u] = t < wn ? op.load(s.y + w0 + t, w0 + t == 0) : Op::dummy();
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int t = t0 + u * SUBW + lane;
+        if (t < wn + kStagePad) items[t] = tmp[u];
+      }
+    }
     __syncwarp(mask);
     int end_w = cur_end - w0;  // current row's end, relative to the window
 #pragma unroll
