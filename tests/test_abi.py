@@ -73,3 +73,36 @@ def test_product_path_fails_loudly_without_cuda(monkeypatch):
     e = st.parse("C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
     with pytest.raises(_abi.ExtensionUnavailable):
         st.run(e)
+
+
+def test_sparse_sparse_argument_validation_without_gpu():
+    """SpGEMM / element-wise entry points reject bad arguments before touching the device."""
+    lib = _abi.load_library()
+    rc = lib.stc_csr_ewise_symbolic(7, 4, 8, 8, 8, 8, 8, 8, 1 << 20, None)
+    assert rc == _abi.STC_EINVAL and b"element-wise op" in lib.stc_last_error()
+    rc = lib.stc_csr_ewise_f32(_abi.EWISE_UNION, -1, 8, 8, 8, 8, 8, 8, 8, 8, 8, None)
+    assert rc == _abi.STC_EINVAL and b"negative" in lib.stc_last_error()
+    rc = lib.stc_csr_ewise_symbolic(_abi.EWISE_INTERSECT, 4, None, 8, 8, 8, 8, 8, 1 << 20, None)
+    assert rc == _abi.STC_EINVAL and b"null" in lib.stc_last_error()
+    rc = lib.stc_spgemm_products(-3, 8, 8, 8, 8, 8, 1 << 20, None)
+    assert rc == _abi.STC_EINVAL
+    # wide B (expand-sort-compress path) with more products than int32 can index
+    assert lib.stc_spgemm_workspace_bytes(10, 100000, 1 << 40) == 0
+    rc = lib.stc_spgemm_symbolic(10, 100000, 8, 8, 8, 8, 8, 8, 8, 1 << 40, 8, 1 << 20, 8, None)
+    assert rc == _abi.STC_EUNSUPPORTED and b"int32" in lib.stc_last_error()
+    rc = lib.stc_spgemm_numeric(10, 16, 8, 8, 8, 8, 8, 8, 5, None, 0, 8, 8, 8, None)
+    assert rc == _abi.STC_EINVAL and b"null" in lib.stc_last_error()
+
+
+def test_sparse_sparse_ops_fail_loudly_without_cuda():
+    import torch
+
+    import paper_2405_16883_b200 as st
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    A = st.build_from_entries((2, 2), st.csr(2, 2), [((0, 1), 1.0)], name="A", device="cpu")
+    B = st.build_from_entries((2, 2), st.csr(2, 2), [((1, 0), 2.0)], name="B", device="cpu")
+    for src in ("C(i,k) = A(i,j) * B(j,k)", "C(i,j) = A(i,j) + B(i,j)", "C(i,j) = A(i,j) * B(i,j)"):
+        with pytest.raises(_abi.ExtensionUnavailable):
+            st.run(st.parse(src, {"A": A, "B": B}))
