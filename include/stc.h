@@ -83,11 +83,16 @@ int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_
  * partial last wave idles SMs. `kind` 0 = SpMM, 1 = MTTKRP.                  */
 int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind);
 
-/* Plan of the COLTILE variant: per row, the first entry of every 128-column
- * chunk of A (int32, stc_coltile_plan_ints(m, n) values). Pass it as the
- * `partition` argument of a COLTILE SpMM.                                    */
-long long stc_coltile_plan_ints(int m, int n);
-int stc_coltile_plan(int m, int n, const int* rowptr, const int* colidx, int* chunk_ptr, void* stream);
+/* Plan of the COLTILE variant (B operand staged in Tensor Memory): A re-encoded
+ * per (128-row block, 64-column chunk, row) as packed {operand offset, value}
+ * entries, each row padded with zero-weight entries to a multiple of 4.
+ * The plan CARRIES A's VALUES (the prepared form of A, like a cuSPARSE SpMM
+ * preprocess): rebuild it whenever the values change. stc_coltile_plan_ints
+ * gives its size in int32 (-1 if unsupported); pass it as the `partition` of a
+ * COLTILE SpMM with the same m, n, nnz (colidx / vals are then not read).    */
+long long stc_coltile_plan_ints(int m, int n, long long nnz);
+int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, const int* colidx, const float* vals,
+                     int* plan, long long plan_ints, void* stream);
 
 /* Workspace for the MERGE variant (carry buffers + per-CTA arrival counters);
  * 0 for ROW/COLTILE. It must be ZERO-FILLED once when allocated; every launch

@@ -1,47 +1,74 @@
-// K3: column-tiled CSR SpMM for wide dense operands (sm_100a).
+// K3: column-tiled CSR SpMM with the dense operand staged in Tensor Memory (sm_100a).
 //
 // C[r, c0:c0+128] = sum_p val[p] * B[col[p], c0:c0+128] for a block of 128 rows.
 //
-// The dense operand is streamed through shared memory in CT_CHUNK-row chunks by
-// a cp.async ring (L2 -> SMEM, bypassing L1); each staged row is reused by every
-// row of the block that holds that column (~12.8 at 10% density), so L2 traffic
-// is (rows/128) x |B[:, tile]| instead of nnz x 512 B of gathers. A plan-time
-// table (`coltile_plan_kernel`) stores, per row, where each chunk's entries
-// start, so a warp reads exactly the entries of (row, chunk) with one coalesced
-// load — no searching, no dependent shuffles. 16 warps own 8 rows x 128 columns
-// of accumulators each (lane = float4). Per entry the weight and column arrive
-// by a broadcast LDS.64 from a per-warp scratch, the operand by one LDS.128, and
-// four FFMAs consume them: the SMEM crossbar (about five wavefronts per entry)
-// bounds the kernel near a quarter of the FP32 FMA peak.
+// Operand path:  global --bulk copy (TMA engine, producer warp)--> SMEM stage (64 B rows x 512 B)
+//                --LDS.128 + tcgen05.st (each lane quarter's 4 warps)--> TMEM
+//                --tcgen05.ld.32x32b.x4--> registers (lane l: B[j, c0+4l .. c0+4l+3])
+// Each staged row is reused by every row of the block holding that column (~12.8
+// at 10 % density). Reading the operand from TMEM takes it off the SMEM crossbar,
+// which caps an SMEM-staged kernel near a quarter of the FP32 peak (the previous
+// design, tools/experiments/coltile_smem.cuh: cfg3 6.41 ms; this kernel: 5.10 ms).
+// No MMA is issued — tensor cores stay off this path (north star); TMEM serves as
+// a wide operand buffer for CUDA-core FMAs.
+//
+// Entry path: the plan (`stc_coltile_plan`) re-encodes A per (128-row block,
+// 64-column chunk, row) as packed entries {4 * (col - chunk start), value bits},
+// each row padded with zero-weight entries to a multiple of 4. A warp's list for
+// a chunk is contiguous: it is copied into SMEM with cp.async one chunk ahead, and
+// the inner loop is two LDS.128 (4 entries) + 4 tcgen05.ld + one wait::ld + 16 FFMA.
+// The plan carries the VALUES of A (it is the prepared form of the matrix, like a
+// cuSPARSE SpMM preprocess): rebuild it when the values change.
+//
+// Pipeline (1 CTA/SM, TMEM = 2 buffers x 256 columns):
+//   producer warp  : bulk copies (TMA engine, one per 512-byte B row) of chunk c -> SMEM stage
+//                    c % 3 once all consumers copied chunk c - 3 out of it (mbarrier `sempty`);
+//                    completion by transaction count on mbarrier `sfull`
+//   16 consumer    : wait `sfull`, copy their 16 rows of chunk c+1 into their lane quarter,
+//   warps            consume chunk c, then a named barrier per quarter (4 warps)
 #pragma once
 
 #include "stc_common.cuh"
 
 namespace stc {
 
-constexpr int CT_ROWS = 128;        // rows per CTA
-constexpr int CT_COLS = 128;        // output columns per CTA (32 lanes x float4)
-constexpr int CT_CHUNK = 128;       // staged B rows per stage
-constexpr int CT_STAGES = 3;
-constexpr int CT_WARPS = 16;
-constexpr int CT_THREADS = CT_WARPS * 32;
-constexpr int CT_RPW = CT_ROWS / CT_WARPS;  // rows per warp
-constexpr size_t CT_STAGE_FLOATS = (size_t)CT_CHUNK * CT_COLS;
-constexpr int CT_SCRATCH = 256;     // staged (col, val) entries per warp and chunk
-constexpr size_t CT_SMEM = CT_STAGES * CT_STAGE_FLOATS * sizeof(float) + (size_t)CT_WARPS * CT_SCRATCH * 8;
+constexpr int CTT_ROWS = 128;
+constexpr int CTT_COLS = 128;
+constexpr int CTT_CHUNK = 64;
+constexpr int CTT_WARPS = 16;                      // consumer warps; one more warp produces
+constexpr int CTT_THREADS = (CTT_WARPS + 1) * 32;
+constexpr int CTT_STAGES = 3;
+constexpr int CTT_RPW = CTT_ROWS / CTT_WARPS;     // rows per consumer warp
+constexpr int CTT_PAD = 4;                        // row segments padded to this many entries
+constexpr int CTT_ECAP = 128;                     // staged entries per warp and chunk
+constexpr size_t CTT_STAGE_FLOATS = (size_t)CTT_CHUNK * CTT_COLS;
+constexpr size_t CTT_SMEM = CTT_STAGES * CTT_STAGE_FLOATS * sizeof(float)  // B stages
+                            + (size_t)CTT_WARPS * 2 * CTT_ECAP * 8          // entry lists (double)
+                            + 128;                                          // barriers, TMEM address
 
-// Plan: chunk_ptr[row * (n_chunks + 1) + c] = first entry of `row` with col >= c * CT_CHUNK.
-__global__ void coltile_plan_kernel(int m, int n_chunks, const int* __restrict__ rowptr,
-                                    const int* __restrict__ colidx, int* __restrict__ chunk_ptr) {
+STC_DEVICE uint32_t ctt_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+STC_DEVICE void ctt_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// ---- plan -----------------------------------------------------------------------------------
+// chunk_ptr[row * (n_chunks + 1) + c] = first entry of `row` with col >= c * CTT_CHUNK
+__global__ void ctt_chunk_ptr_kernel(int m, int n_chunks, const int* __restrict__ rowptr,
+                                     const int* __restrict__ colidx, int* __restrict__ chunk_ptr) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= m) return;
   const int a = rowptr[row], b = rowptr[row + 1];
   int* out = chunk_ptr + (long long)row * (n_chunks + 1);
   for (int c = lane; c <= n_chunks; c += 32) {
-    // lower_bound of c*CT_CHUNK in colidx[a, b)
     int lo = a, hi = b;
-    const int key = c * CT_CHUNK;
+    const int key = c * CTT_CHUNK;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (colidx[mid] < key)
@@ -53,176 +80,225 @@ __global__ void coltile_plan_kernel(int m, int n_chunks, const int* __restrict__
   }
 }
 
-
-// Per-warp offsets of its CT_RPW rows' entries within one chunk: lane r (< CT_RPW)
-// knows start(r), lane CT_RPW + r knows end(r); returns the exclusive prefix of the
-// counts for row `lane % CT_RPW` and the total.
-STC_DEVICE void chunk_layout(int bounds, int lane, int& my_off, int& total) {
-  const int other = __shfl_xor_sync(0xffffffffu, bounds, CT_RPW);  // end for lanes < CT_RPW
-  int cnt = (lane < CT_RPW) ? other - bounds : 0;
-  int incl = cnt;
-#pragma unroll
-  for (int d = 1; d < CT_RPW; d <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += t;
+// padded entry count of every (block, chunk, row-in-block) slot; slot order = list order
+__global__ void ctt_count_kernel(int m, int n_chunks, long long n_slots, const int* __restrict__ chunk_ptr,
+                                 int* __restrict__ counts) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_slots;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int rr = (int)(i % CTT_ROWS);
+    const long long bc = i / CTT_ROWS;
+    const int c = (int)(bc % n_chunks);
+    const int row = (int)(bc / n_chunks) * CTT_ROWS + rr;
+    int cnt = 0;
+    if (row < m) {
+      const int* cp = chunk_ptr + (long long)row * (n_chunks + 1) + c;
+      cnt = (cp[1] - cp[0] + CTT_PAD - 1) / CTT_PAD * CTT_PAD;
+    }
+    counts[i] = cnt;
   }
-  my_off = incl - cnt;
-  total = __shfl_sync(0xffffffffu, incl, CT_RPW - 1);
 }
 
-constexpr int CT_PREF = CT_SCRATCH / 32;  // prefetched items per lane
+__global__ void ctt_scatter_kernel(int m, int n_chunks, const int* __restrict__ chunk_ptr,
+                                   const int* __restrict__ colidx, const float* __restrict__ vals,
+                                   const int* __restrict__ offs, int2* __restrict__ ent) {
+  const long long n_pairs = (long long)m * n_chunks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pairs;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / n_chunks), c = (int)(i % n_chunks);
+    const int* cp = chunk_ptr + (long long)row * (n_chunks + 1) + c;
+    const int a = cp[0], b = cp[1];
+    const long long slot = ((long long)(row / CTT_ROWS) * n_chunks + c) * CTT_ROWS + row % CTT_ROWS;
+    int e = offs[slot];
+    for (int p = a; p < b; ++p) ent[e++] = make_int2(4 * (colidx[p] - c * CTT_CHUNK), __float_as_int(vals[p]));
+    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(0, 0);
+  }
+}
 
+// ---- kernel ---------------------------------------------------------------------------------
 template <int EPI, bool ADD>
-__global__ void __launch_bounds__(CT_THREADS, 1) coltile_kernel(int m, int n, int k, const int* __restrict__ chunk_ptr,
-                                                               const int* __restrict__ colidx,
-                                                               const float* __restrict__ vals,
-                                                               const float* __restrict__ B, long long ldb,
-                                                               float* __restrict__ C, long long ldc,
-                                                               const float* __restrict__ D, long long ldd) {
-  extern __shared__ __align__(16) float smem[];  // [CT_STAGES][CT_CHUNK][CT_COLS] + per-warp scratch
+__global__ void __launch_bounds__(CTT_THREADS, 1)
+    coltile_tmem_kernel(int m, int n, int k, const int* __restrict__ offs, const int2* __restrict__ ent,
+                        const float* __restrict__ B, long long ldb, float* __restrict__ C, long long ldc,
+                        const float* __restrict__ D, long long ldd) {
+  extern __shared__ __align__(1024) float smem[];
+  int2* lists = reinterpret_cast<int2*>(smem + CTT_STAGES * CTT_STAGE_FLOATS);  // [warp][2][ECAP]
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(lists + CTT_WARPS * 2 * CTT_ECAP);
+  uint64_t* sempty = sfull + CTT_STAGES;
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(sempty + CTT_STAGES);
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int row_base = blockIdx.x * CT_ROWS + warp * CT_RPW;
-  const int c0 = blockIdx.y * CT_COLS;
-  const int col = c0 + lane * 4;
-  const int n_chunks = (n + CT_CHUNK - 1) / CT_CHUNK;
-  int2* scratch = reinterpret_cast<int2*>(smem + CT_STAGES * CT_STAGE_FLOATS) + warp * CT_SCRATCH;
+  const int c0 = blockIdx.y * CTT_COLS;
+  const int n_chunks = (n + CTT_CHUNK - 1) / CTT_CHUNK;
 
-  float acc[CT_RPW][4];
-#pragma unroll
-  for (int r = 0; r < CT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
-
-  auto stage = [&](int chunk) {
-    const int j0 = chunk * CT_CHUNK;
-    float* dst = smem + (chunk % CT_STAGES) * CT_STAGE_FLOATS;
-#pragma unroll
-    for (int t = 0; t < (int)(CT_STAGE_FLOATS / 4) / CT_THREADS; ++t) {
-      const int idx = threadIdx.x + t * CT_THREADS;
-      const int jr = idx / 32, cq = idx % 32;
-      const int j = j0 + jr;
-      const int cc = c0 + cq * 4;
-      const bool ok = (j < n) && (cc < k);
-      cp_async16(dst + jr * CT_COLS + cq * 4, ok ? (const void*)(B + (long long)j * ldb + cc) : (const void*)B, ok);
-    }
-  };
-
-  // lane r (< CT_RPW) reads the chunk start of row r, lane CT_RPW + r its end
-  const int prow = row_base + (lane % CT_RPW);
-  const bool prow_ok = lane < 2 * CT_RPW && prow < m;
-  const int* cp_row = chunk_ptr + (long long)prow * (n_chunks + 1) + (lane >= CT_RPW ? 1 : 0);
-  auto load_bounds = [&](int ch) { return (prow_ok && ch < n_chunks) ? ld_stream(cp_row + ch) : 0; };
-
-  // prefetch of one chunk's entries into registers: item idx = t*32 + lane of the
-  // concatenation of the warp's rows' entry ranges
-  int pc[CT_PREF];
-  float pv[CT_PREF];
-  auto prefetch = [&](int bnd) {
-    int my_off, total;
-    chunk_layout(bnd, lane, my_off, total);
-    int offs[CT_RPW], starts[CT_RPW];
-#pragma unroll
-    for (int r = 0; r < CT_RPW; ++r) {  // row r owns items [offs[r], offs[r+1])
-      offs[r] = __shfl_sync(0xffffffffu, my_off, r);
-      starts[r] = __shfl_sync(0xffffffffu, bnd, r);
-    }
-#pragma unroll
-    for (int t = 0; t < CT_PREF; ++t) {
-      const int idx = t * 32 + lane;
-      pc[t] = INT_MAX;
-      pv[t] = 0.f;
-      if (idx < total) {
-        int pos = 0;
-#pragma unroll
-        for (int r = 0; r < CT_RPW; ++r)
-          if (idx >= offs[r]) pos = starts[r] + (idx - offs[r]);
-        pc[t] = ld_stream(colidx + pos);
-        pv[t] = ld_stream(vals + pos);
-      }
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s < CT_STAGES - 1; ++s) {
-    if (s < n_chunks) stage(s);
-    cp_async_commit();
+  if (warp == 0) {  // TMEM: 512 columns = two 256-column buffers
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(ctt_smem_u32(tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  int b_cur = load_bounds(0);
-  int b_next = load_bounds(1);
-  prefetch(b_cur);
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    const int b_after = load_bounds(ch + 2);
-    const int j0 = ch * CT_CHUNK;
-    // publish this chunk's prefetched entries (column relative to the chunk)
-#pragma unroll
-    for (int t = 0; t < CT_PREF; ++t)
-      if (pc[t] != INT_MAX) scratch[t * 32 + lane] = make_int2(pc[t] - j0, __float_as_int(pv[t]));
-    cp_async_wait<CT_STAGES - 2>();
-    __syncthreads();  // chunk ch staged for all; the slot refilled below is no longer read
-    if (ch + CT_STAGES - 1 < n_chunks) stage(ch + CT_STAGES - 1);
-    cp_async_commit();
-    int my_off, total;
-    chunk_layout(b_cur, lane, my_off, total);
-    prefetch(b_next);  // next chunk's entries stream in while this one is consumed
-    const float* tile = smem + (ch % CT_STAGES) * CT_STAGE_FLOATS + lane * 4;
-#pragma unroll
-    for (int r = 0; r < CT_RPW; ++r) {
-      const int o0 = __shfl_sync(0xffffffffu, my_off, r);
-      const int o1 = r + 1 < CT_RPW ? __shfl_sync(0xffffffffu, my_off, r + 1) : total;
-      const int a = __shfl_sync(0xffffffffu, b_cur, r);
-      int q = o0;
-      const int qe = min(o1, CT_SCRATCH);
-      for (; q + 4 <= qe; q += 4) {
-        int2 it[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) it[u] = scratch[q + u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 x = *reinterpret_cast<const float4*>(tile + it[u].x * CT_COLS);
-          const float w = __int_as_float(it[u].y);
-          acc[r][0] = fmaf(w, x.x, acc[r][0]);
-          acc[r][1] = fmaf(w, x.y, acc[r][1]);
-          acc[r][2] = fmaf(w, x.z, acc[r][2]);
-          acc[r][3] = fmaf(w, x.w, acc[r][3]);
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < CTT_STAGES; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ctt_smem_u32(&sfull[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ctt_smem_u32(&sempty[b])), "r"(CTT_WARPS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = *tbase_s;
+
+  if (warp == CTT_WARPS) {
+    // ---------------- producer: B chunks -> SMEM stages (bulk copies, one per B row) ----------------
+    const int row_bytes = 4 * min(CTT_COLS, k - c0);  // multiple of 16 (k % 4 == 0)
+    for (int c = 0; c < n_chunks; ++c) {
+      const int s = c % CTT_STAGES;
+      if (c >= CTT_STAGES) ctt_mbar_wait(ctt_smem_u32(&sempty[s]), (uint32_t)((c / CTT_STAGES - 1) & 1));
+      const int j0 = c * CTT_CHUNK;
+      const int rows = min(CTT_CHUNK, n - j0);
+      float* dst = smem + s * CTT_STAGE_FLOATS;
+      if (rows < CTT_CHUNK || row_bytes < 4 * CTT_COLS) {  // zero what the copies do not cover
+        for (int idx = lane; idx < (int)(CTT_STAGE_FLOATS / 4); idx += 32) {
+          const int jr = idx / 32, cq = idx % 32;
+          if (jr >= rows || 16 * cq >= row_bytes)
+            *reinterpret_cast<float4*>(dst + jr * CTT_COLS + cq * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      const uint32_t bar = ctt_smem_u32(&sfull[s]);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * row_bytes)
+                     : "memory");
+      __syncwarp();
+      for (int jr = lane; jr < rows; jr += 32)  // the warp's lanes issue the row copies in parallel
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                ctt_smem_u32(dst + jr * CTT_COLS)),
+            "l"(B + (long long)(j0 + jr) * ldb + c0), "r"(row_bytes), "r"(bar)
+            : "memory");
+    }
+  } else {
+    // ---------------- consumers: 8 rows x 128 columns each ----------------
+    const int row_base = blockIdx.x * CTT_ROWS + warp * CTT_RPW;
+    const int quarter = warp % 4, part = warp / 4;
+    const uint32_t tq = tbase + ((uint32_t)(32 * quarter) << 16);  // this warp's TMEM lane quarter
+    int2* mylists = lists + warp * 2 * CTT_ECAP;
+    const int* offs_w = offs + (long long)blockIdx.x * n_chunks * CTT_ROWS + warp * CTT_RPW;
+    // lanes 0..CTT_RPW: the warp's row boundaries in the padded list of chunk ch
+    auto load_meta = [&](int ch) {
+      return (lane <= CTT_RPW && ch < n_chunks) ? ld_stream(offs_w + (long long)ch * CTT_ROWS + lane) : 0;
+    };
+    auto stage_list = [&](int ch, int meta) {  // cp.async of chunk ch's list (skipped if it overflows)
+      if (ch < n_chunks) {
+        const int e0 = __shfl_sync(0xffffffffu, meta, 0);
+        const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
+        if (total <= CTT_ECAP) {
+          int2* dst = mylists + (ch & 1) * CTT_ECAP;
+          for (int i = lane; i < total / 2; i += 32) cp_async16(dst + 2 * i, ent + e0 + 2 * i, true);
         }
       }
-      for (; q < qe; ++q) {
-        const int2 it = scratch[q];
-        const float4 x = *reinterpret_cast<const float4*>(tile + it.x * CT_COLS);
-        const float w = __int_as_float(it.y);
-        acc[r][0] = fmaf(w, x.x, acc[r][0]);
-        acc[r][1] = fmaf(w, x.y, acc[r][1]);
-        acc[r][2] = fmaf(w, x.z, acc[r][2]);
-        acc[r][3] = fmaf(w, x.w, acc[r][3]);
+      cp_async_commit();
+    };
+    auto fill = [&](int c) {  // this warp's 16 B rows of chunk c -> its TMEM lane quarter
+      ctt_mbar_wait(ctt_smem_u32(&sfull[c % CTT_STAGES]), (uint32_t)((c / CTT_STAGES) & 1));
+      constexpr int kRows = CTT_CHUNK / 4;
+      const float* src = smem + (c % CTT_STAGES) * CTT_STAGE_FLOATS + (kRows * part) * CTT_COLS + lane * 4;
+      const uint32_t dst = tq + (uint32_t)((c & 1) * 4 * CTT_CHUNK + 4 * kRows * part);
+#pragma unroll 8
+      for (int j = 0; j < kRows; ++j) {  // (unrolled: loads run ahead of the TMEM stores)
+        const float4 v = *reinterpret_cast<const float4*>(src + j * CTT_COLS);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + 4 * j),
+                     "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                     "r"(__float_as_uint(v.w))
+                     : "memory");
       }
-      // overflow beyond the scratch capacity (dense rows): read entries directly
-      for (int qq = max(o0, CT_SCRATCH); qq < o1; ++qq) {
-        const int pos = a + (qq - o0);
-        const float4 x = *reinterpret_cast<const float4*>(tile + (colidx[pos] - j0) * CT_COLS);
-        const float w = vals[pos];
-        acc[r][0] = fmaf(w, x.x, acc[r][0]);
-        acc[r][1] = fmaf(w, x.y, acc[r][1]);
-        acc[r][2] = fmaf(w, x.z, acc[r][2]);
-        acc[r][3] = fmaf(w, x.w, acc[r][3]);
-      }
-    }
-    __syncwarp();  // scratch is rewritten at the top of the next chunk
-    b_cur = b_next;
-    b_next = b_after;
-  }
-  cp_async_wait<0>();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[c % CTT_STAGES])) : "memory");
+    };
+    auto quarter_sync = [&]() {
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    };
+
+    float acc[CTT_RPW][4];
 #pragma unroll
-  for (int r = 0; r < CT_RPW; ++r) {
-    const int row = row_base + r;
-    if (row < m && col < k) {
-      float4 o = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
-      if constexpr (ADD) {
-        const float4 d = *reinterpret_cast<const float4*>(D + (long long)row * ldd + col);
-        o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
+    for (int r = 0; r < CTT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
+    // 4 entries -> 4 tcgen05.ld, one wait, 16 FFMA
+    auto group = [&](float (&a)[4], uint32_t tchunk, int4 e01, int4 e23) {
+      uint32_t x[4][4];
+      const int cols[4] = {e01.x, e01.z, e23.x, e23.z};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
+                     : "r"(tchunk + (uint32_t)cols[u]));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const float w[4] = {__int_as_float(e01.y), __int_as_float(e01.w), __int_as_float(e23.y),
+                          __int_as_float(e23.w)};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[0] = fmaf(w[u], __uint_as_float(x[u][0]), a[0]);
+        a[1] = fmaf(w[u], __uint_as_float(x[u][1]), a[1]);
+        a[2] = fmaf(w[u], __uint_as_float(x[u][2]), a[2]);
+        a[3] = fmaf(w[u], __uint_as_float(x[u][3]), a[3]);
       }
-      o.x = act<EPI>(o.x); o.y = act<EPI>(o.y); o.z = act<EPI>(o.z); o.w = act<EPI>(o.w);
-      st_stream4(C + (long long)row * ldc + col, o);
+    };
+
+    int meta = load_meta(0);
+    int meta_next = load_meta(1);
+    stage_list(0, meta);
+    if (n_chunks > 0) fill(0);
+    quarter_sync();
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      const int meta_after = load_meta(ch + 2);
+      stage_list(ch + 1, meta_next);
+      cp_async_wait<1>();  // chunk ch's list has landed (ch + 1's may be in flight)
+      __syncwarp();
+      if (ch + 1 < n_chunks) fill(ch + 1);
+      const uint32_t tchunk = tq + (uint32_t)((ch & 1) * 4 * CTT_CHUNK);
+      const int e0 = __shfl_sync(0xffffffffu, meta, 0);
+      const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
+      if (total <= CTT_ECAP) {
+        const int4* sc = reinterpret_cast<const int4*>(mylists + (ch & 1) * CTT_ECAP);
+#pragma unroll
+        for (int r = 0; r < CTT_RPW; ++r) {
+          const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
+          const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
+          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], tchunk, sc[q / 2], sc[q / 2 + 1]);
+        }
+      } else {  // rows denser than the staged list: entries straight from global memory
+        const int4* g = reinterpret_cast<const int4*>(ent + e0);
+#pragma unroll
+        for (int r = 0; r < CTT_RPW; ++r) {
+          const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
+          const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
+          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], tchunk, g[q / 2], g[q / 2 + 1]);
+        }
+      }
+      quarter_sync();  // chunk ch fully read, chunk ch + 1 fully written
+      meta = meta_next;
+      meta_next = meta_after;
+    }
+    cp_async_wait<0>();
+    const int col = c0 + lane * 4;
+#pragma unroll
+    for (int r = 0; r < CTT_RPW; ++r) {
+      const int row = row_base + r;
+      if (row < m && col < k) {
+        float4 o = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        if constexpr (ADD) {
+          const float4 d = *reinterpret_cast<const float4*>(D + (long long)row * ldd + col);
+          o.x += d.x; o.y += d.y; o.z += d.z; o.w += d.w;
+        }
+        o.x = act<EPI>(o.x); o.y = act<EPI>(o.y); o.z = act<EPI>(o.z); o.w = act<EPI>(o.w);
+        st_stream4(C + (long long)row * ldc + col, o);
+      }
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
 }  // namespace stc

@@ -99,20 +99,46 @@ int dispatch_spmm(int epilogue, bool add, const SegOut& o, const MergeShape& ms,
              : dispatch_subw<VEC, EPI_NONE, false>(subw, o, ms, op, L);
 }
 
+// ---- COLTILE plan: header {magic, n_chunks} | padded offsets | counts | chunk_ptr | CUB temp |
+// packed entries (int2, 16-byte aligned). See coltile.cuh.
+struct CttLayout {
+  int n_chunks;
+  long long n_slots, max_entries;
+  size_t temp_bytes;
+  long long offs, counts, chunk_ptr, temp, ent, total_ints;
+};
+inline CttLayout ctt_layout(int m, int n, long long nnz) {
+  CttLayout l{};
+  l.n_chunks = (int)ceil_div(n, CTT_CHUNK);
+  l.n_slots = ceil_div(m, CTT_ROWS) * l.n_chunks * CTT_ROWS;
+  l.max_entries = nnz + (long long)(CTT_PAD - 1) * std::min<long long>(nnz, (long long)m * l.n_chunks);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int*)nullptr, (int*)nullptr, (int)(l.n_slots + 1));
+  l.temp_bytes = tb;
+  auto up4 = [](long long x) { return (x + 3) / 4 * 4; };
+  l.offs = 4;
+  l.counts = up4(l.offs + l.n_slots + 1);
+  l.chunk_ptr = up4(l.counts + l.n_slots + 1);
+  l.temp = up4(l.chunk_ptr + (long long)m * (l.n_chunks + 1));
+  l.ent = up4(l.temp + (long long)((tb + 3) / 4));
+  l.total_ints = l.ent + 2 * std::max<long long>(l.max_entries, 1);
+  return l;
+}
+
 template <int EPI, bool ADD>
-int launch_coltile(int m, int n, int k, const int* chunk_ptr, const int* colidx, const float* vals,
-                   const float* B, long long ldb, float* C, long long ldc, const float* D, long long ldd,
-                   cudaStream_t st, const Launch& L) {
+int launch_coltile_tmem(int m, int n, int k, long long nnz, const int* plan, const float* B, long long ldb, float* C,
+                        long long ldc, const float* D, long long ldd, cudaStream_t st, const Launch& L) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(coltile_kernel<EPI, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM);
+    cudaFuncSetAttribute(coltile_tmem_kernel<EPI, ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTT_SMEM);
     configured = true;
   }
   if (m == 0 || k == 0) return STC_OK;
-  const dim3 grid((unsigned)ceil_div(m, CT_ROWS), (unsigned)ceil_div(k, CT_COLS));
-  launch_windowed(coltile_kernel<EPI, ADD>, grid, dim3(CT_THREADS), CT_SMEM, st, L.window, L.window_bytes, m, n,
-                  k, chunk_ptr, colidx, vals, B, ldb, C, ldc, D, ldd);
-  return check_launch("coltile_kernel");
+  const CttLayout lay = ctt_layout(m, n, nnz);
+  const dim3 grid((unsigned)ceil_div(m, CTT_ROWS), (unsigned)ceil_div(k, CTT_COLS));
+  launch_windowed(coltile_tmem_kernel<EPI, ADD>, grid, dim3(CTT_THREADS), CTT_SMEM, st, L.window, L.window_bytes, m,
+                  n, k, plan + lay.offs, reinterpret_cast<const int2*>(plan + lay.ent), B, ldb, C, ldc, D, ldd);
+  return check_launch("coltile_tmem_kernel");
 }
 
 // Shared validation + dispatch for every SpMM-shaped entry point.
@@ -134,17 +160,16 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
                     (!D || (ldd % 4 == 0 && aligned16(D))) && (val_bs % 4 == 0 || batch == 1) &&
                     (b_bs % 4 == 0) && (c_bs % 4 == 0);
 
-  if (variant == STC_VARIANT_COLTILE) {
+  if (variant == STC_VARIANT_COLTILE) {  // operand staged in Tensor Memory; the plan carries A
     if (!vec4) return fail(STC_EUNSUPPORTED, "COLTILE needs k, ldb, ldc multiples of 4 and 16-byte alignment");
     if (batch != 1) return fail(STC_EUNSUPPORTED, "COLTILE is not batched");
     if (!partition) return fail(STC_EINVAL, "COLTILE needs its plan (stc_coltile_plan) as `partition`");
     const Launch L{variant, 1, st, B, (size_t)((long long)n * ldb) * sizeof(float)};
-    const int* cp = partition;
     if (epilogue == STC_EPILOGUE_RELU)
-      return D ? launch_coltile<EPI_RELU, true>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L)
-               : launch_coltile<EPI_RELU, false>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L);
-    return D ? launch_coltile<EPI_NONE, true>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L)
-             : launch_coltile<EPI_NONE, false>(m, n, k, cp, colidx, vals, B, ldb, C, ldc, D, ldd, st, L);
+      return D ? launch_coltile_tmem<EPI_RELU, true>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L)
+               : launch_coltile_tmem<EPI_RELU, false>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L);
+    return D ? launch_coltile_tmem<EPI_NONE, true>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L)
+             : launch_coltile_tmem<EPI_NONE, false>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L);
   }
   if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
     return fail(STC_EINVAL, "unknown variant %d", variant);
@@ -248,19 +273,38 @@ extern "C" int stc_merge_plan_items_per_group(int m, long long nnz, int k, int b
   }
 }
 
-extern "C" long long stc_coltile_plan_ints(int m, int n) {
-  if (m < 0 || n < 0) return -1;
-  return (long long)m * (ceil_div(n, CT_CHUNK) + 1);
+extern "C" long long stc_coltile_plan_ints(int m, int n, long long nnz) {
+  if (m < 0 || n < 0 || nnz < 0) return -1;
+  const CttLayout lay = ctt_layout(m, n, nnz);
+  if (lay.max_entries >= INT32_MAX) return -1;
+  return lay.total_ints;
 }
 
-extern "C" int stc_coltile_plan(int m, int n, const int* rowptr, const int* colidx, int* chunk_ptr, void* stream) {
-  if (m < 0 || n < 0) return fail(STC_EINVAL, "negative extent");
+extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, const int* colidx,
+                                const float* vals, int* plan, long long plan_ints, void* stream) {
+  if (m < 0 || n < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
+  if (!plan || !rowptr || (nnz && (!colidx || !vals))) return fail(STC_EINVAL, "null pointer");
+  const CttLayout lay = ctt_layout(m, n, nnz);
+  if (lay.max_entries >= INT32_MAX) return fail(STC_EUNSUPPORTED, "COLTILE plan exceeds int32 entries");
+  if (plan_ints < lay.total_ints)
+    return fail(STC_EINVAL, "plan buffer of %lld ints, need %lld", plan_ints, lay.total_ints);
   if (m == 0) return STC_OK;
-  if (!rowptr || !chunk_ptr) return fail(STC_EINVAL, "null pointer");
-  const int n_chunks = (int)ceil_div(n, CT_CHUNK);
-  coltile_plan_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      m, n_chunks, rowptr, colidx, chunk_ptr);
-  return check_launch("coltile_plan_kernel");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* chunk_ptr = plan + lay.chunk_ptr;
+  int* counts = plan + lay.counts;
+  int* offs = plan + lay.offs;
+  ctt_chunk_ptr_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(m, lay.n_chunks, rowptr, colidx, chunk_ptr);
+  if (int rc = check_launch("ctt_chunk_ptr_kernel")) return rc;
+  ctt_count_kernel<<<1184, 256, 0, st>>>(m, lay.n_chunks, lay.n_slots, chunk_ptr, counts);
+  if (int rc = check_launch("ctt_count_kernel")) return rc;
+  cudaMemsetAsync(counts + lay.n_slots, 0, sizeof(int), st);
+  size_t tb = lay.temp_bytes;
+  const cudaError_t e =
+      cub::DeviceScan::ExclusiveSum(plan + lay.temp, tb, counts, offs, (int)(lay.n_slots + 1), st);
+  if (e != cudaSuccess) return fail(STC_ELAUNCH, "coltile plan scan: %s", cudaGetErrorString(e));
+  ctt_scatter_kernel<<<1184, 256, 0, st>>>(m, lay.n_chunks, chunk_ptr, colidx, vals, offs,
+                                           reinterpret_cast<int2*>(plan + lay.ent));
+  return check_launch("ctt_scatter_kernel");
 }
 
 extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {

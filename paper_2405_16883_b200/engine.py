@@ -428,7 +428,8 @@ def _spmm_rows(ctx: _Ctx, m: _SpmmTerm, addend: torch.Tensor | None = None, relu
     if variant == "merge":
         partition = _partition(A, view, key, K)
     elif variant == "coltile":
-        partition = _cache(A, ("coltile",) + key, lambda: ops.coltile_plan(view.rowptr, view.cols, Bd.shape[0]))
+        partition = _cache(A, ("coltile",) + key,
+                           lambda: ops.coltile_plan(view.rowptr, view.cols, Bd.shape[0], view.vals))
     if addend is not None and not view.dense_rows:
         raise UnsupportedExpressionError("dense addend with a compressed row level")
     Y = ops.spmm_csr(view.rowptr, view.cols, view.vals, Bd, addend=addend, relu=relu,

@@ -125,19 +125,28 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
 
 @dataclass
 class ColtilePlan:
-    """Per-row chunk starts for the COLTILE variant (int32 [m, n_chunks + 1])."""
+    """Prepared form of A for the COLTILE variant (int32 buffer, see include/stc.h).
 
-    chunk_ptr: torch.Tensor
+    It carries A's values: build it from the same (rowptr, colidx, vals) the SpMM
+    is called with, and rebuild it when the values change. The engine caches it per
+    tensor, which is safe because tensors are immutable (`tensor.py:53-56`).
+    """
+
+    plan: torch.Tensor
+    nnz: int
 
 
-def coltile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, n_cols: int) -> ColtilePlan:
-    require_cuda(rowptr, colidx)
+def coltile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, n_cols: int, vals: torch.Tensor) -> ColtilePlan:
+    require_cuda(rowptr, colidx, vals)
     m = rowptr.numel() - 1
-    ints = int(lib().stc_coltile_plan_ints(m, n_cols))
-    cp = torch.empty(max(ints, 1), dtype=torch.int32, device=rowptr.device)
-    check(lib().stc_coltile_plan(m, n_cols, ptr(rowptr), ptr(colidx), ptr(cp), stream_handle()),
-          "stc_coltile_plan")
-    return ColtilePlan(cp)
+    nnz = int(colidx.numel())
+    ints = int(lib().stc_coltile_plan_ints(m, n_cols, nnz))
+    if ints < 0:
+        raise ValueError(f"COLTILE plan unsupported for m={m} n={n_cols} nnz={nnz}")
+    plan = torch.empty(max(ints, 1), dtype=torch.int32, device=rowptr.device)
+    check(lib().stc_coltile_plan(m, n_cols, nnz, ptr(_i32(rowptr)), ptr(_i32(colidx)), ptr(_f32(vals)), ptr(plan),
+                                 ints, stream_handle()), "stc_coltile_plan")
+    return ColtilePlan(plan, nnz)
 
 
 def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int, batch: int,
@@ -190,8 +199,10 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
         if workspace is None:
             workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
     elif variant == "coltile":
-        partition = partition or coltile_plan(rowptr, colidx, n)
-        plan_ptr = ptr(partition.chunk_ptr)
+        partition = partition or coltile_plan(rowptr, colidx, n, vals)
+        if partition.nnz != nnz:
+            raise ValueError(f"COLTILE plan built for nnz={partition.nnz}, matrix has {nnz}")
+        plan_ptr = ptr(partition.plan)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_spmm_csr_f32(
         m, n, k, ptr(rowptr), ptr(colidx), ptr(vals), nnz, ptr(B), B.stride(0), ptr(out),
