@@ -48,6 +48,7 @@ struct SpmmOp {
 
   static constexpr int kRing = 8;           // gathers in flight per group
   static constexpr int kMinBlocks = 4;      // resident CTAs per SM (register budget)
+  static constexpr int kStageUnroll = 8;    // item loads per lane in flight while staging
   static constexpr int kStageBytes = 32768;  // staged items per CTA (rest of SMEM stays L1)
   struct Item {
     unsigned off;
@@ -93,6 +94,7 @@ struct MttkrpOp {
   // B[j,:] once per fiber (flag = first entry of a fiber) instead of once per entry.
   static constexpr int kRing = VEC == 4 ? 4 : 8;
   static constexpr int kMinBlocks = 3;
+  static constexpr int kStageUnroll = 1;     // (2 and 3 measured: no gain, more registers)
   static constexpr int kStageBytes = 32768;  // 3 CTAs x 50 KB SMEM leaves ~75 KB of L1 for the hot factor rows
   struct __align__(16) Item {
     unsigned offb, offc;
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     const int wn = min(CAP, n_nnz - w0);
     __syncwarp(mask);
     // SU loads per lane in flight before their SMEM stores (one latency per SU * SUBW items)
-    constexpr int SU = sizeof(Item) <= 8 ? 8 : 1;
+    constexpr int SU = Op::kStageUnroll;
     for (int t0 = 0; t0 < wn + kStagePad; t0 += SU * SUBW) {
       Item tmp[SU];
 #pragma unroll
