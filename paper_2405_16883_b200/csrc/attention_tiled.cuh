@@ -39,23 +39,30 @@ struct TileArgs {
 };
 
 // ---------------------------------------------------------------------------
-// attn_tile8_kernel (64 threads).
+// attn_tile8_kernel<TXN> (8 * TXN threads; shipped with TXN = 16: 128 threads).
 //
-// Thread (ty, tx) = (tid / 8, tid % 8) owns rows {4ty..4ty+3, 32+4ty..32+4ty+3} and
-// columns / head dims {4tx..4tx+3, 32+4tx..32+4tx+3}: per 4-wide slice of the
-// reduction it issues 16 LDS.128 for 256 FMAs (a 4x4 tiling of 256 threads: 8 for
-// 64, and SMEM-wavefront bound at 40 % FMA-pipe use — measured, cfg4 0.85 ms). Q, K and V are staged by
+// Thread (ty, tx) = (tid / TXN, tid % TXN) owns rows {4ty..4ty+3, 32+4ty..32+4ty+3} and
+// 64 / TXN columns / head dims (4tx..4tx+3, and 32+4tx.. when TXN = 8): per 4-wide slice
+// of the reduction TXN = 16 issues 12 LDS.128 for 128 FMAs, TXN = 8 16 for 256 (a 4x4
+// tiling of 256 threads: 8 for 64, SMEM-wavefront bound at 40 % FMA-pipe use — cfg4
+// 0.85 ms; TXN = 8: 0.80 ms, 255 registers, 6 warps/SM; TXN = 16: 0.77 ms, 16 warps/SM). Q, K and V are staged by
 // cp.async (K and V of tile t+1 once tile t is done; P^T reuses K's buffer so that
 // four CTAs fit an SM and cover each other's copies). K rows are stored with
 // their 16-byte chunks XOR-swizzled by (row / 4) % 8 and P^T with its row chunks
 // swizzled the same way, so the 8 lanes of a quarter-warp hit 8 bank groups.
 // ---------------------------------------------------------------------------
-constexpr int AT8_THREADS = 64;
 constexpr size_t AT8_SMEM = 3ull * AT_B * AT_B * sizeof(float);  // Qs, Ks (aliased by Pt), Vs
 
+// TXN threads share a row: TXN = 8 -> 8x8 register tiles (64 threads), TXN = 16 -> 8x4 (128 threads).
+// Column / head-dim j of thread tx: (j / 4) * 4 * TXN + 4 * tx + j % 4.
+template <int TXN>
+STC_DEVICE int at8_col(int tx, int j) { return (j / 4) * 4 * TXN + 4 * tx + (j % 4); }
 STC_DEVICE int at8_row(int ty, int i) { return i < 4 ? 4 * ty + i : 32 + 4 * ty + (i - 4); }
 
-__global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) {
+template <int TXN>
+__global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
+  constexpr int NT = 8 * TXN;   // threads
+  constexpr int CW = 64 / TXN;  // columns (and head dims) per thread
   extern __shared__ __align__(16) float sm8[];
   float* Qs = sm8;                  // [row][d]
   float* Ks = Qs + AT_B * AT_B;     // [col][d], chunk-swizzled
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
   float* Pt = Ks;                   // [col][row], row-chunk swizzled (K is dead once S is done)
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x;
-  const int tx = tid % 8, ty = tid / 8;
+  const int tx = tid % TXN, ty = tid / TXN;
   const int row0 = b * AT_B;
   const float* Qh = a.Q + h * a.q_hs;
   const float* Kh = a.K + h * a.k_hs;
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
   const int* cols = a.tile_cols + (long long)b * a.dt_max;
 
   auto stage_rows = [&](float* dst, const float* src, long long rs, int r0, int limit, bool swz) {
-    for (int idx = tid; idx < AT_B * 16; idx += AT8_THREADS) {
+    for (int idx = tid; idx < AT_B * 16; idx += NT) {
       const int r = idx / 16, dq = idx % 16;
       const bool ok = r0 + r < limit;
       const int slot = swz ? (dq ^ ((r >> 2) & 7)) : dq;
@@ -88,37 +95,37 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
     stage_rows(Vs, Vh, a.v_rs, cols[0] * AT_B, a.n, false);
   }
 
-  float o[8][8], mrow[8], lrow[8];
+  float o[8][CW], mrow[8], lrow[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     mrow[i] = -INFINITY;
     lrow[i] = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[i][e] = 0.f;
+    for (int e = 0; e < CW; ++e) o[i][e] = 0.f;
   }
 
   for (int t = 0; t < n_t; ++t) {
     cp_async_wait<1>();  // Q and K(t) landed; V(t) may still be in flight
     __syncthreads();
-    float s[8][8];
+    float s[8][CW];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s[i][j] = 0.f;
+      for (int j = 0; j < CW; ++j) s[i][j] = 0.f;
 #pragma unroll 1
     for (int dq = 0; dq < 16; ++dq) {
-      float4 q4[8], k4[8];
+      float4 q4[8], k4[CW];
 #pragma unroll
       for (int i = 0; i < 8; ++i) q4[i] = *reinterpret_cast<const float4*>(Qs + at8_row(ty, i) * AT_D + dq * 4);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = at8_row(tx, j);
+      for (int j = 0; j < CW; ++j) {
+        const int c = at8_col<TXN>(tx, j);
         k4[j] = *reinterpret_cast<const float4*>(Ks + c * AT_D + ((dq ^ ((c >> 2) & 7)) * 4));
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < CW; ++j) {
           s[i][j] = fmaf(q4[i].x, k4[j].x, s[i][j]);
           s[i][j] = fmaf(q4[i].y, k4[j].y, s[i][j]);
           s[i][j] = fmaf(q4[i].z, k4[j].z, s[i][j]);
@@ -131,36 +138,39 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = at8_row(ty, i);
-      const float4 m0 = ld_stream4(mv_tile + r * AT_B + 4 * tx);
-      const float4 m1 = ld_stream4(mv_tile + r * AT_B + 32 + 4 * tx);
-      const float mva[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      float mva[CW];
+#pragma unroll
+      for (int jq = 0; jq < CW / 4; ++jq) {
+        const float4 m4 = ld_stream4(mv_tile + r * AT_B + at8_col<TXN>(tx, 4 * jq));
+        mva[4 * jq] = m4.x; mva[4 * jq + 1] = m4.y; mva[4 * jq + 2] = m4.z; mva[4 * jq + 3] = m4.w;
+      }
       float tmax = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < CW; ++j) {
         s[i][j] = isnan(mva[j]) ? -INFINITY : s[i][j] * mva[j] * a.scale;
         tmax = fmaxf(tmax, s[i][j]);
       }
 #pragma unroll
-      for (int w = 4; w >= 1; w >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, w));
+      for (int w = TXN / 2; w >= 1; w >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, w));
       const float mnew = fmaxf(mrow[i], tmax);
       const float corr = (mnew == -INFINITY) ? 1.f : expf(mrow[i] - mnew);
       float rsum = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < CW; ++j) {
         s[i][j] = (s[i][j] == -INFINITY) ? 0.f : expf(s[i][j] - mnew);
         rsum += s[i][j];
       }
 #pragma unroll
-      for (int w = 4; w >= 1; w >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, w);
+      for (int w = TXN / 2; w >= 1; w >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, w);
       lrow[i] = lrow[i] * corr + rsum;
       mrow[i] = mnew;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[i][e] *= corr;
+      for (int e = 0; e < CW; ++e) o[i][e] *= corr;
     }
     // P^T: column c, row chunk rc (4 rows) stored at chunk rc ^ ((c >> 2) & 7)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = at8_row(tx, j);
+    for (int j = 0; j < CW; ++j) {
+      const int c = at8_col<TXN>(tx, j);
       const int sw = (c >> 2) & 7;
       *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * (ty ^ sw)) = make_float4(s[0][j], s[1][j], s[2][j], s[3][j]);
       *reinterpret_cast<float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw)) =
@@ -173,14 +183,17 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
       const int sw = (c >> 2) & 7;
       const float4 pa = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ sw));
       const float4 pb = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw));
-      const float4 va = *reinterpret_cast<const float4*>(Vs + c * AT_D + 4 * tx);
-      const float4 vb = *reinterpret_cast<const float4*>(Vs + c * AT_D + 32 + 4 * tx);
       const float p8[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-      const float v8[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+      float v8[CW];
+#pragma unroll
+      for (int eq = 0; eq < CW / 4; ++eq) {
+        const float4 v4 = *reinterpret_cast<const float4*>(Vs + c * AT_D + at8_col<TXN>(tx, 4 * eq));
+        v8[4 * eq] = v4.x; v8[4 * eq + 1] = v4.y; v8[4 * eq + 2] = v4.z; v8[4 * eq + 3] = v4.w;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
+        for (int e = 0; e < CW; ++e) o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
     }
     __syncthreads();  // done with Vs and Pt: stream in the next tile's K and V
     if (t + 1 < n_t) {
@@ -194,8 +207,10 @@ __global__ void __launch_bounds__(AT8_THREADS, 4) attn_tile8_kernel(TileArgs a) 
     const int row = row0 + at8_row(ty, i);
     if (row >= a.m) continue;
     float* dst = a.Opart + ((long long)h * a.m + row) * AT_D;
-    *reinterpret_cast<float4*>(dst + 4 * tx) = make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
-    *reinterpret_cast<float4*>(dst + 32 + 4 * tx) = make_float4(o[i][4], o[i][5], o[i][6], o[i][7]);
+#pragma unroll
+    for (int eq = 0; eq < CW / 4; ++eq)
+      *reinterpret_cast<float4*>(dst + at8_col<TXN>(tx, 4 * eq)) =
+          make_float4(o[i][4 * eq], o[i][4 * eq + 1], o[i][4 * eq + 2], o[i][4 * eq + 3]);
     if (tx == 0) a.ml[(long long)h * a.m + row] = make_float2(mrow[i], lrow[i]);
   }
 }
