@@ -201,7 +201,16 @@ def _dense_torch(t: Tensor, order) -> torch.Tensor:
         else to_torch(t)
     if tuple(order) != tuple(range(t.order)):
         x = x.permute(*order)
-    return x.contiguous()
+    x = x.contiguous()
+    # torch calls a permuted view with size-1 dims contiguous without fixing their strides;
+    # the kernels read the innermost stride, so give every dim its canonical stride
+    want, acc = [], 1
+    for d in reversed(x.shape):
+        want.append(acc)
+        acc *= d
+    if tuple(reversed(want)) != x.stride():
+        x = x.clone(memory_format=torch.contiguous_format)
+    return x
 
 
 def _dense_result(name: str, arr: torch.Tensor) -> Tensor:
@@ -441,7 +450,12 @@ def _spmm_rows(ctx: _Ctx, m: _SpmmTerm, addend: torch.Tensor | None = None, relu
 def _spmm_counters(ctx: _Ctx, m: _SpmmTerm, view: RowView, K: int):
     nnz = view.vals.numel()
     if m.k is None:  # SpMV: scalar path (engine.py:515-531 not taken)
-        ctx.counter.add(nnz, nnz + view.n_rows, 2 * nnz)
+        if view.kind == "csr":
+            ctx.counter.add(nnz, nnz + view.n_rows, 2 * nnz)
+        elif view.kind in ("coo", "dcsr"):  # workspace per distinct row
+            ctx.counter.add(nnz, nnz + view.n_segments, 3 * view.n_segments + 2 * nnz)
+        else:  # column-major storage walked [j, i]
+            ctx.counter.add(nnz, nnz, 2 * nnz)
         return
     order = ctx.sched.loop_order
     nblk = _n_blocks(K, ctx.sched, m.k)
@@ -513,18 +527,27 @@ def _exec_dense_output(ctx: _Ctx) -> Tensor:
 
 
 def _dense_einsum(ctx: _Ctx, term, out_vars) -> torch.Tensor:
+    """One all-dense term over the output's index space. Output indices the term does
+    not mention are broadcast (the reference's eval_dense adds the term's value at
+    every such coordinate, oracle.py:35-46)."""
     letters = {}
     for v in list(out_vars) + [v for a in term for v in a.indices]:
         letters.setdefault(v, string.ascii_letters[len(letters)])
+    term_vars = {v for a in term for v in a.indices}
+    present = [v for v in out_vars if v in term_vars]
     subs = ",".join("".join(letters[v] for v in a.indices) for a in term)
-    eq = f"{subs}->{''.join(letters[v] for v in out_vars)}"
+    eq = f"{subs}->{''.join(letters[v] for v in present)}"
     ops_ = [_dense_torch(ctx.t(a), tuple(range(a.tensor.order))) for a in term]
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     try:
-        return torch.einsum(eq, *ops_).to(torch.float32)
+        r = torch.einsum(eq, *ops_).to(torch.float32)
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
+    if len(present) != len(out_vars):
+        shape = [ctx.extents[v] if v in term_vars else 1 for v in out_vars]
+        r = r.reshape(shape).expand(*[ctx.extents[v] for v in out_vars]).contiguous()
+    return r
 
 
 def _exec_batched_pv(ctx: _Ctx, pv: _BatchedPvTerm) -> torch.Tensor:
@@ -678,7 +701,9 @@ def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
 def _exec_sparse_spmm(ctx: _Ctx, m: _SpmmTerm) -> Tensor:
     """SpMM whose inferred output is [compressed i, dense k] (COO / DCSR / CSC operands)."""
     out_vars = ctx.expr.output_indices
-    if m.k is None or list(out_vars) != [m.i, m.k]:
+    if m.k is None:
+        return _exec_sparse_spmv(ctx, m)
+    if list(out_vars) != [m.i, m.k]:
         raise UnsupportedExpressionError("sparse-output SpMM must be spelled C(i,k)")
     if ctx.out_fmt.levels != (LevelFormat.COMPRESSED, LevelFormat.DENSE) or \
             ctx.out_fmt.mode_ordering != (0, 1):
@@ -695,6 +720,26 @@ def _exec_sparse_spmm(ctx: _Ctx, m: _SpmmTerm) -> Tensor:
     else:
         rows = view.seg_rows
     return _compressed_dense_result(ctx.expr.output_name, (view.n_rows, K), rows, Y)
+
+
+def _exec_sparse_spmv(ctx: _Ctx, m: _SpmmTerm) -> Tensor:
+    """SpMV whose inferred output is a compressed vector over the rows that hold entries
+    (COO / DCSR / CSC operands; the reference's 1-D workspace drain)."""
+    if ctx.out_fmt.levels != (LevelFormat.COMPRESSED,):
+        raise UnsupportedExpressionError(f"SpMV into {ctx.out_fmt.name()} is not supported on the device")
+    view, Y, K = _spmm_rows(ctx, m)
+    _spmm_counters(ctx, m, view, K)
+    if view.dense_rows:
+        lens = view.rowptr[1:] - view.rowptr[:-1]
+        rows = torch.nonzero(lens > 0).flatten().to(torch.int32)
+        Y = Y[rows.long()]
+    else:
+        rows = view.seg_rows
+    n = rows.numel()
+    pos = torch.tensor([0, n], dtype=torch.int32, device=Y.device)
+    st_ = TensorStorage(ctx.out_fmt, (CompressedLevel(pos, rows.to(torch.int32).contiguous()),),
+                        Y.reshape(-1).contiguous())
+    return Tensor(ctx.expr.output_name, (view.n_rows,), st_)
 
 
 # ---------------------------------------------------------------------------

@@ -387,6 +387,23 @@ def ewise_mul_csr():
     return run_case("ewise_mul_csr", "C(i,j) = A(i,j) * B(i,j)", {"A": A, "B": B})
 
 
+@case
+def spmv_coo():
+    # SpMV with a COO matrix: compressed-vector output over the rows holding entries
+    rng = np.random.default_rng(123)
+    A = st.build_from_entries((27, 19), st.coo(27, 19), rand_sparse_entries(rng, (27, 19), 0.1, 0.05), "A")
+    x = st.from_dense(f32(rng.uniform(-1, 1, 19)), name="x")
+    return run_case("spmv_coo", "y(i) = A(i,j) * x(j)", {"A": A, "x": x})
+
+
+@case
+def spmv_csc():
+    rng = np.random.default_rng(124)
+    A = st.build_from_entries((21, 16), st.csc(21, 16), rand_sparse_entries(rng, (21, 16), 0.15), "A")
+    x = st.from_dense(f32(rng.uniform(-1, 1, 16)), name="x")
+    return run_case("spmv_csc", "y(i) = A(i,j) * x(j)", {"A": A, "x": x})
+
+
 def main():
     only = set(sys.argv[1:])
     index = {}
