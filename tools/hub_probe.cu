@@ -9,7 +9,24 @@
 #include <cuda_runtime.h>
 
 // grid-stride over chunks of `per_warp` indices; rows < H come from shared memory
-template <int U>
+template <int POL>
+__device__ __forceinline__ float4 ldp(const float4* p) {
+  float4 v;
+  if constexpr (POL == 0) {
+    v = __ldg(p);
+  } else if constexpr (POL == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  } else if constexpr (POL == 2) {
+    asm volatile("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  } else if constexpr (POL == 3) {
+    v = __ldcg(p);
+  } else {
+    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  }
+  return v;
+}
+
+template <int U, int POL = 0>
 __global__ void gather_hub(const float4* __restrict__ table, const int* __restrict__ idx, long long n_idx,
                            int per_warp, int H, float* __restrict__ out) {
   extern __shared__ float4 hub[];
@@ -32,7 +49,7 @@ __global__ void gather_hub(const float4* __restrict__ table, const int* __restri
           int r = __shfl_sync(0xffffffffu, my, (q0 + u) & 31);
           if (q0 + u >= n) v[u] = make_float4(0, 0, 0, 0);
           else if (r < H) v[u] = hub[r * 32 + lane];
-          else v[u] = __ldg(table + (size_t)r * 32 + lane);
+          else v[u] = ldp<POL>(table + (size_t)r * 32 + lane);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
@@ -43,21 +60,22 @@ __global__ void gather_hub(const float4* __restrict__ table, const int* __restri
 }
 
 static float* g_flush = nullptr;
+static size_t g_reserve = 0;
 
-template <int U>
+template <int U, int POL = 0>
 float run(const float4* t, const int* idx, long long n, int per_warp, int threads, int per_sm, int H, float* out) {
-  const size_t smem = (size_t)H * 512;
-  cudaFuncSetAttribute(gather_hub<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const size_t smem = (size_t)H * 512 + g_reserve;
+  cudaFuncSetAttribute(gather_hub<U, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   const int blocks = 148 * per_sm;
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int w = 0; w < 3; ++w) gather_hub<U><<<blocks, threads, smem>>>(t, idx, n, per_warp, H, out);
+  for (int w = 0; w < 3; ++w) gather_hub<U, POL><<<blocks, threads, smem>>>(t, idx, n, per_warp, H, out);
   const int reps = 10;
   float total = 0;
   for (int r = 0; r < reps; ++r) {
     cudaMemsetAsync(g_flush, r, 512ull << 20);
     cudaEventRecord(a);
-    gather_hub<U><<<blocks, threads, smem>>>(t, idx, n, per_warp, H, out);
+    gather_hub<U, POL><<<blocks, threads, smem>>>(t, idx, n, per_warp, H, out);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
@@ -144,7 +162,7 @@ int main(int argc, char** argv) {
   float* out; cudaMalloc(&out, 64 << 20);
   const double gb = m * 512.0 / 1e9;
   struct Cfg { int threads, per_sm, H; };
-  for (Cfg c : {Cfg{256, 4, 0}, Cfg{256, 8, 0}}) {
+  for (Cfg c : {Cfg{256, 4, 0}, Cfg{256, 6, 0}, Cfg{256, 8, 0}}) {
     for (int pw : {32, 128}) {
       float m8 = run<8>(table, di, m, pw, c.threads, c.per_sm, c.H, out);
       float m16 = run<16>(table, di, m, pw, c.threads, c.per_sm, c.H, out);
@@ -152,7 +170,22 @@ int main(int argc, char** argv) {
              c.per_sm, c.H, pw, m8 * 1e3, gb / (m8 * 1e-3), m16 * 1e3, gb / (m16 * 1e-3));
     }
   }
+  // shared memory reserved but unused (shrinks L1 like the merge kernel's staging does)
+  for (int rsv_kb : {0, 16, 32, 46, 56}) {
+    g_reserve = rsv_kb * 1024;
+    printf("reserve %2d KB/CTA x4: U8 %.1f us\n", rsv_kb, 1e3 * run<8, 0>(table, di, m, 32, 256, 4, 0, out));
+  }
+  g_reserve = 0;
+  for (int pw : {32, 128}) {
+    printf("policy per_warp %3d: U8 ldg %.1f  no_alloc %.1f  evict_first %.1f  cg %.1f  evict_last %.1f | U4 ldg %.1f no_alloc %.1f cg %.1f | U6 ldg %.1f us\n", pw,
+           1e3 * run<8, 0>(table, di, m, pw, 256, 4, 0, out), 1e3 * run<8, 1>(table, di, m, pw, 256, 4, 0, out),
+           1e3 * run<8, 2>(table, di, m, pw, 256, 4, 0, out), 1e3 * run<8, 3>(table, di, m, pw, 256, 4, 0, out),
+           1e3 * run<8, 4>(table, di, m, pw, 256, 4, 0, out), 1e3 * run<4, 0>(table, di, m, pw, 256, 4, 0, out),
+           1e3 * run<4, 1>(table, di, m, pw, 256, 4, 0, out), 1e3 * run<4, 3>(table, di, m, pw, 256, 4, 0, out),
+           1e3 * run<6, 0>(table, di, m, pw, 256, 4, 0, out));
+  }
   struct CCfg { int threads, per_sm; };
+  if (argc > 2)
   for (CCfg c : {CCfg{256, 4}, CCfg{256, 3}, CCfg{256, 2}, CCfg{512, 1}, CCfg{512, 2}}) {
     for (int pw : {32, 128}) {
       const int warps = c.threads / 32 * c.per_sm;
