@@ -35,7 +35,14 @@ def eval_dense(e: TensorExpr, bindings: dict | None = None) -> np.ndarray:
             operands.append(to_torch(t).to(torch.float64))
             subs.append("".join(letters.setdefault(v, string.ascii_letters[len(letters)])
                                 for v in a.indices))
-        eq = ",".join(subs) + "->" + "".join(letters[v] for v in e.output_indices)
+        # output indices the term does not mention: the term's value is added at every
+        # such coordinate (oracle.py:35-46 loops over all output coordinates)
+        term_vars = {v for a in term for v in a.indices}
+        present = [v for v in e.output_indices if v in term_vars]
+        eq = ",".join(subs) + "->" + "".join(letters[v] for v in present)
         r = torch.einsum(eq, *operands)
+        if len(present) != len(e.output_indices):
+            shape = [s if v in term_vars else 1 for v, s in zip(e.output_indices, e.output_shape)]
+            r = r.reshape(shape).expand(*e.output_shape)
         out = r if out is None else out + r
     return out.cpu().numpy()

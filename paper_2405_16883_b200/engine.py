@@ -40,6 +40,7 @@ import torch
 from . import ops
 from .expr import Access, TensorExpr, get_index_variables, index_extents
 from .format_inference import infer_format
+from .generic import TooLargeForGenericWalk, execute_generic
 from .formats import LevelFormat, TensorFormat, dense_format
 from .scheduler import CostModel, Schedule, schedule, schedule_to_dict
 from .tensor import (
@@ -826,11 +827,26 @@ def _exec_ewise(ctx: _Ctx, op: str, a: Access, b: Access) -> Tensor:
 
 
 def _dispatch(ctx: _Ctx) -> Tensor:
+    """Dedicated kernel when the expression matches one; otherwise the device loop-nest
+    walker (`generic.py`), which follows the reference interpreter's iteration space."""
+    e = ctx.expr
+    if ctx.out_fmt.shape != e.output_shape:
+        raise ShapeError(f"output format shape {ctx.out_fmt.shape} != expression output {e.output_shape}")
+    _require_device(ctx.tensor_of.values())
+    try:
+        return _dispatch_kernels(ctx)
+    except UnsupportedExpressionError as err:
+        ctx.counter = OpCounter()
+        ctx.chosen = [f"generic:device-walk ({err})"[:160]]
+        try:
+            return execute_generic(ctx.sched, ctx.tensor_of, ctx.out_fmt, ctx.counter)
+        except TooLargeForGenericWalk as big:
+            raise UnsupportedExpressionError(f"{err}; generic walk: {big}") from None
+
+
+def _dispatch_kernels(ctx: _Ctx) -> Tensor:
     e = ctx.expr
     out_fmt = ctx.out_fmt
-    if out_fmt.shape != e.output_shape:
-        raise ShapeError(f"output format shape {out_fmt.shape} != expression output {e.output_shape}")
-    _require_device(ctx.tensor_of.values())
     terms = e.terms()
     out_vars = e.output_indices
     if not out_fmt.has_sparse_levels:

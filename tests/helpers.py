@@ -119,6 +119,11 @@ def abs_bound(e, tensors):
         for a in term:
             ops.append(np.abs(st.to_dense(tensors[a.tensor.name])))
             subs.append("".join(letters.setdefault(v, string.ascii_letters[len(letters)]) for v in a.indices))
-        r = np.einsum(",".join(subs) + "->" + "".join(letters[v] for v in e.output_indices), *ops)
+        term_vars = {v for a in term for v in a.indices}
+        present = [v for v in e.output_indices if v in term_vars]
+        r = np.einsum(",".join(subs) + "->" + "".join(letters[v] for v in present), *ops)
+        if len(present) != len(e.output_indices):  # broadcast over output indices the term lacks
+            shape = [s if v in term_vars else 1 for v, s in zip(e.output_indices, e.output_shape)]
+            r = np.broadcast_to(r.reshape(shape), e.output_shape)
         out = r if out is None else out + r
     return out

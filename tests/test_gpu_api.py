@@ -83,7 +83,8 @@ def test_rebinding():
         st.execute(s, bindings={"A": st.convert(A1, st.dcsr(50, 40))})
 
 
-def test_unsupported_raises_no_fallback():
+def test_expressions_without_a_kernel_run_on_the_device_walker():
+    """No dedicated kernel -> the device loop-nest walker (generic.py), never the CPU."""
     r = np.random.default_rng(1)
     from helpers import random_tensor
 
@@ -91,15 +92,30 @@ def test_unsupported_raises_no_fallback():
     B = random_tensor(r, (6, 6), "csr", 0.3, "B")
     D = random_tensor(r, (6, 6), "csr", 0.3, "D")
     Ad = random_tensor(r, (6, 6), "dcsr", 0.3, "Ad")
-    with pytest.raises(st.UnsupportedExpressionError):  # three sparse factors
-        st.run(st.parse("C(i,j) = A(i,j) * B(i,j) * D(i,j)", {"A": A, "B": B, "D": D}))
-    with pytest.raises(st.UnsupportedExpressionError):  # three sparse terms
-        st.run(st.parse("C(i,j) = A(i,j) + B(i,j) + D(i,j)", {"A": A, "B": B, "D": D}))
-    with pytest.raises(st.UnsupportedExpressionError):  # SpGEMM needs CSR operands
-        st.run(st.parse("C(i,k) = Ad(i,j) * B(j,k)", {"Ad": Ad, "B": B}))
     Bd = st.from_dense(r.uniform(-1, 1, (6, 4)), name="Bd")
-    with pytest.raises(st.UnsupportedExpressionError):
-        st.run(st.parse("C(i,k) = A(i,j) * Bd(j,k)", {"A": A, "Bd": Bd}), out_format=st.csr(6, 4))
+    cases = [
+        ("C(i,j) = A(i,j) * B(i,j) * D(i,j)", {"A": A, "B": B, "D": D}, None),   # three sparse factors
+        ("C(i,j) = A(i,j) + B(i,j) + D(i,j)", {"A": A, "B": B, "D": D}, None),   # three sparse terms
+        ("C(i,k) = Ad(i,j) * B(j,k)", {"Ad": Ad, "B": B}, None),                 # DCSR x CSR SpGEMM
+        ("C(i,k) = A(i,j) * Bd(j,k)", {"A": A, "Bd": Bd}, st.csr(6, 4)),         # forced CSR output
+    ]
+    for src, b, fmt in cases:
+        e = st.parse(src, b)
+        out, _, report = st.run_with_report(e, out_format=fmt)
+        assert out.storage.values.is_cuda
+        assert report["variants"] and report["variants"][0].startswith("generic:device-walk"), report
+        assert out.format == (fmt or st.infer_format(e))
+        np.testing.assert_allclose(st.to_dense(out), st.eval_dense(e), rtol=1e-6, atol=1e-6)
+
+
+def test_walk_too_large_raises():
+    n = 200_000
+    x = st.from_arrays((n,), st.TensorFormat((n,), (0,), (st.LevelFormat.COMPRESSED,)),
+                       np.arange(n)[:, None], np.ones(n), name="x", device="cuda")
+    y = st.from_arrays((n,), st.TensorFormat((n,), (0,), (st.LevelFormat.COMPRESSED,)),
+                       np.arange(n)[:, None], np.ones(n), name="y", device="cuda")
+    with pytest.raises(st.UnsupportedExpressionError):  # 4e10 outer-product entries
+        st.run(st.parse("G(i,j) = x(i) * y(j)", {"x": x, "y": y}))
 
 
 def test_dense_dispatch_matches_hand_results():

@@ -141,10 +141,13 @@ def test_engine_spgemm_and_ewise_through_api():
         assert np.allclose(st.to_dense(out), dense(), atol=1e-5)
 
 
-def test_engine_rejects_non_csr_sparse_sparse():
+def test_non_csr_sparse_sparse_runs_on_the_device_walker():
+    """COO x CSR has no SpGEMM kernel: the device loop-nest walker computes it."""
     rng = np.random.default_rng(12)
     A = st.from_dense((rng.random((10, 8)) < 0.3) * 1.0, st.coo(10, 8), name="A")
     B = st.from_dense((rng.random((8, 9)) < 0.3) * 1.0, st.csr(8, 9), name="B")
     e = st.parse("C(i,k) = A(i,j) * B(j,k)", {"A": A, "B": B})
-    with pytest.raises(NotImplementedError):
-        st.run(e)
+    out, _, report = st.run_with_report(e)
+    assert report["variants"][0].startswith("generic:device-walk")
+    assert out.format == st.infer_format(e)
+    assert np.allclose(st.to_dense(out), st.to_dense(A) @ st.to_dense(B), atol=1e-6)
