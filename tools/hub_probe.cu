@@ -145,6 +145,70 @@ float run_cp(const float4* t, const int* idx, long long n, int per_warp, int thr
   return total / reps;
 }
 
+// 256-bit loads: a half-warp covers a 512-byte row (8 floats per lane), so one warp
+// instruction gathers two rows (indices q and q+1 of the warp's chunk); U pairs in flight
+__device__ __forceinline__ void ld256(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+template <int U>
+__global__ void gather256(const float* __restrict__ table, const int* __restrict__ idx, long long n_idx,
+                          int per_warp, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const long long warps_total = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (long long w = warp0; w * per_warp < n_idx; w += warps_total) {
+    const long long p0 = w * per_warp;
+    const long long p1 = min(p0 + per_warp, n_idx);
+    for (long long b = p0; b < p1; b += 32) {
+      int my = (b + lane < p1) ? idx[b + lane] : -1;
+      int n = (int)min(32LL, p1 - b);
+      for (int q0 = 0; q0 < n; q0 += 2 * U) {
+        float v[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + 2 * u + half;
+          int r = __shfl_sync(0xffffffffu, my, q & 31);
+          if (q < n) ld256(table + (size_t)r * 128 + hl * 8, v[u]);
+          else { for (int e = 0; e < 8; ++e) v[u][e] = 0.f; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += v[u][e];
+      }
+    }
+  }
+  float t = 0;
+  for (int e = 0; e < 8; ++e) t += acc[e];
+  out[warp0 * 32 + lane] = t;
+}
+
+template <int U>
+float run256(const float* t, const int* idx, long long n, int per_warp, int threads, int per_sm, float* out) {
+  const int blocks = 148 * per_sm;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int w = 0; w < 3; ++w) gather256<U><<<blocks, threads>>>(t, idx, n, per_warp, out);
+  const int reps = 10;
+  float total = 0;
+  for (int r = 0; r < reps; ++r) {
+    cudaMemsetAsync(g_flush, r, 512ull << 20);
+    cudaEventRecord(a);
+    gather256<U><<<blocks, threads>>>(t, idx, n, per_warp, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    total += ms;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) printf("error: %s\n", cudaGetErrorString(e));
+  return total / reps;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) { printf("usage: hub_probe colidx.bin\n"); return 1; }
   cudaMalloc(&g_flush, 512ull << 20);
@@ -169,6 +233,13 @@ int main(int argc, char** argv) {
       printf("thr %4d x%d/SM H %3d per_warp %3d: U8 %6.1f us (%6.0f GB/s)  U16 %6.1f us (%6.0f GB/s)\n", c.threads,
              c.per_sm, c.H, pw, m8 * 1e3, gb / (m8 * 1e-3), m16 * 1e3, gb / (m16 * 1e-3));
     }
+  }
+  for (int pw : {32, 64, 128}) {
+    printf("256-bit per_warp %3d: U2 %.1f  U4 %.1f  U8 %.1f us  | x8/SM U4 %.1f\n", pw,
+           1e3 * run256<2>((const float*)table, di, m, pw, 256, 4, out),
+           1e3 * run256<4>((const float*)table, di, m, pw, 256, 4, out),
+           1e3 * run256<8>((const float*)table, di, m, pw, 256, 4, out),
+           1e3 * run256<4>((const float*)table, di, m, pw, 256, 8, out));
   }
   // shared memory reserved but unused (shrinks L1 like the merge kernel's staging does)
   for (int rsv_kb : {0, 16, 32, 46, 56}) {
