@@ -104,6 +104,8 @@ size_t stc_spmm_workspace_bytes(int m, long long nnz, int k, int variant, int it
  * Replaces the dense-output driver + vectorised tail of the reference,
  * engine.py:487-573 (`_run_dense_output`, `vector_sink`), for
  * C(i,k) = A(i,j) * B(j,k) [+ D(i,k)] with A CSR, B/D dense.
+ * B of any size: below 2^32 elements the gathers use prepared 32-bit offsets,
+ * at or above it 64-bit addresses (same walk and summation order).
  * n = columns of A (rows of B); D nullable; `partition` = the merge-path
  * starts for MERGE, the chunk plan for COLTILE, ignored for ROW.            */
 int stc_spmm_csr_f32(int m, int n, int k, const int* rowptr, const int* colidx, const float* vals,
@@ -182,7 +184,8 @@ int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, int n_blocks,
 /* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
  * M[s,:] = sum_{p in seg s} vals[p] * B[j[p],:] * C[k[p],:], evaluated fiber by
  * fiber: each run of equal j sums vals * C[k,:] and multiplies by B[j,:] once.
- * B has n_j rows, C has n_k rows (each below 2^32 elements: 32-bit gather offsets).
+ * B has n_j rows, C has n_k rows (below 2^32 elements the gathers use prepared 32-bit
+ * offsets, at or above it 64-bit addresses; any size that fits in memory).
  * Replaces `_run_sparse_output` with the (i,r) Workspace, engine.py:577-644,
  * 71-90, for M(i,r) = T(i,j,k) * B(j,r) * C(k,r).                           */
 int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,

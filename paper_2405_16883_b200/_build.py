@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libstc.so"
-SOURCES = ["abi_common.cu", "spmm.cu", "attention.cu", "spgemm.cu"]
+SOURCES = ["abi_common.cu", "spmm.cu", "spmm_wide.cu", "attention.cu", "spgemm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
@@ -40,19 +40,23 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     nvcc = _nvcc()
-    objs = []
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
-    for src in SOURCES:
-        obj = build_dir / (Path(src).stem + ".o")
-        cmd = [nvcc, *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            sys.stderr.write(res.stdout + res.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(res.stderr)
-        objs.append(str(obj))
+    objs = [str(build_dir / (Path(src).stem + ".o")) for src in SOURCES]
+    cmds = [[nvcc, *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", obj]
+            for src, obj in zip(SOURCES, objs)]
+    # the translation units are independent: compile them concurrently
+    procs = [subprocess.Popen(c, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for c in cmds]
+    failed = None
+    for src, p in zip(SOURCES, procs):
+        out, err = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
+            failed = failed or src
+        elif verbose:
+            sys.stderr.write(err)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -34,9 +34,9 @@ namespace stc {
 // ---------------------------------------------------------------------------
 
 // Items are staged in a "prepared" form: dense-operand row offsets are
-// pre-multiplied by the leading dimension (32-bit element offsets; the C ABI
-// rejects dense operands of 2^32 elements or more), so a gather is one
-// IMAD.WIDE + one LDG.128. `shift(col0)` moves the dense pointers to the
+// pre-multiplied by the leading dimension (32-bit element offsets; dense
+// operands of 2^32 elements or more take the *WideOp forms below), so a gather
+// is one IMAD.WIDE + one LDG.128. `shift(col0)` moves the dense pointers to the
 // lane's first column once per kernel.
 template <int VEC>
 struct SpmmOp {
@@ -153,6 +153,37 @@ struct MttkrpOp {
   }
 };
 
+// 64-bit gathers for dense operands of 2^32 elements or more (e.g. 40 M-node
+// graphs x 128 features, 20 GB): the item keeps the row index and the address is
+// formed in 64 bits at fetch time (one more IMAD per gather than the prepared
+// 32-bit offset). Same walk, carries and summation order as SpmmOp / MttkrpOp.
+template <int VEC>
+struct SpmmWideOp : SpmmOp<VEC> {
+  using Item = typename SpmmOp<VEC>::Item;
+  using Pre = typename SpmmOp<VEC>::Pre;
+  STC_DEVICE Item load(long long p, bool /*first*/) const {
+    return Item{(unsigned)ld_stream(this->col + p), ld_stream(this->val + p)};
+  }
+  STC_DEVICE void fetch(const Item& it, Pre& pre) const {
+    pre.b.load_gather(this->B + (long long)it.off * this->ldb + this->lane_off);
+  }
+};
+
+template <int VEC>
+struct MttkrpWideOp : MttkrpOp<VEC> {
+  using Item = typename MttkrpOp<VEC>::Item;
+  using Pre = typename MttkrpOp<VEC>::Pre;
+  STC_DEVICE Item load(long long p, bool first) const {
+    const int j = ld_stream(this->jc + p);
+    const bool start = first || p == 0 || ld_stream(this->jc + p - 1) != j;
+    return Item{(unsigned)j, (unsigned)ld_stream(this->kc + p), ld_stream(this->val + p), start ? 1 : 0};
+  }
+  STC_DEVICE void fetch(const Item& it, Pre& pre) const {
+    if (it.flag) pre.b.load_gather(this->B + (long long)it.offb * this->ldb + this->lane_off);
+    pre.c.load_gather(this->C + (long long)it.offc * this->ldcf + this->lane_off);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Output/epilogue context
 // ---------------------------------------------------------------------------
@@ -185,8 +216,8 @@ STC_DEVICE void write_row(const SegOut& o, int row, int col0, Frag<VEC> acc) {
 // Plan-time merge-path partition: starts[g] = (row, pos) at diagonal g*IPG.
 // ---------------------------------------------------------------------------
 
-__global__ void merge_partition_kernel(int m, long long nnz, const int* __restrict__ rowptr,
-                                       int ipg, int n_groups, int2* __restrict__ starts) {
+static __global__ void merge_partition_kernel(int m, long long nnz, const int* __restrict__ rowptr,
+                                              int ipg, int n_groups, int2* __restrict__ starts) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g > n_groups) return;
   const long long total = (long long)m + nnz;

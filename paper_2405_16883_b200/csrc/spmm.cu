@@ -6,98 +6,13 @@
 
 #include "abi_util.cuh"
 #include "coltile.cuh"
-#include "segreduce.cuh"
+#include "seg_launch.cuh"
 
 using namespace stc;
 
+using namespace stc::seg;
+
 namespace {
-
-constexpr int kThreads = 256;
-constexpr int kMaxIpg = 1024;  // staged items per group (shared memory bound)
-
-int choose_subw(int k, int vec) {
-  for (int s : {4, 8, 16}) {
-    if (s * vec >= k) return s;
-  }
-  return 32;
-}
-
-long long n_groups_for(int m, long long nnz, int ipg) { return ceil_div((long long)m + nnz, ipg); }
-
-size_t merge_ws_bytes(int m, long long nnz, int k, int subw, int vec, int ipg, int batch) {
-  const long long groups = n_groups_for(m, nnz, ipg);
-  const int ng = kThreads / subw;
-  const long long n_cta = ceil_div(groups, ng);
-  const int sw = subw * vec;
-  const long long slabs = ceil_div(k, sw);
-  return (size_t)(2LL * batch * slabs * n_cta * sw * (long long)sizeof(float) +
-                  batch * slabs * n_cta * (long long)sizeof(int));
-}
-
-struct Launch {
-  int variant;
-  int batch;
-  cudaStream_t stream;
-  const void* window;      // gathered dense operand (L2 access-policy window)
-  size_t window_bytes;
-};
-
-template <int SUBW, int VEC, int EPI, bool ADD, class Op>
-int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
-  constexpr int SW = SUBW * VEC;
-  constexpr int U = SUBW >= 8 ? Op::kRing : 4;
-  const int slabs = (int)ceil_div(o.k, SW);
-  if (o.m == 0 || slabs == 0) return STC_OK;
-  if (L.variant == STC_VARIANT_ROW) {
-    // a row's sub-warp loads SUBW entries at a time: keep up to 16 of their gathers in flight
-    constexpr int UR = SUBW >= 16 ? 16 : (SUBW >= 8 ? 8 : 4);
-    const dim3 grid((unsigned)ceil_div((long long)o.m * SUBW, kThreads), slabs, L.batch);
-    launch_windowed(row_kernel<SUBW, VEC, EPI, ADD, UR, Op>, grid, dim3(kThreads), 0, L.stream, L.window,
-                    L.window_bytes, o, ms, op);
-    return check_launch("row_kernel");
-  }
-  constexpr int NG = kThreads / SUBW;
-  ms.n_cta = (int)ceil_div(ms.n_groups, NG);
-  if (ms.n_cta == 0) return STC_OK;
-  const dim3 grid(ms.n_cta, slabs, L.batch);
-  constexpr size_t smem = merge_smem_bytes<SUBW, VEC, Op>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  if (o.k % SW == 0)
-    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op>, grid, dim3(kThreads), smem, L.stream,
-                    L.window, L.window_bytes, o, ms, op);
-  else
-    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>, grid, dim3(kThreads), smem, L.stream,
-                    L.window, L.window_bytes, o, ms, op);
-  return check_launch("merge_kernel");
-}
-
-template <int VEC, int EPI, bool ADD, template <int> class OpT>
-int dispatch_subw(int subw, const SegOut& o, const MergeShape& ms, const OpT<VEC>& op, const Launch& L) {
-  switch (subw) {
-    case 4: return launch_seg<4, VEC, EPI, ADD>(o, ms, op, L);
-    case 8: return launch_seg<8, VEC, EPI, ADD>(o, ms, op, L);
-    case 16: return launch_seg<16, VEC, EPI, ADD>(o, ms, op, L);
-    default: return launch_seg<32, VEC, EPI, ADD>(o, ms, op, L);
-  }
-}
-
-template <int VEC>
-int dispatch_spmm(int epilogue, bool add, const SegOut& o, const MergeShape& ms, const SpmmOp<VEC>& op,
-                  const Launch& L) {
-  const int subw = choose_subw(o.k, VEC);
-  if (epilogue == STC_EPILOGUE_RELU)
-    return add ? dispatch_subw<VEC, EPI_RELU, true>(subw, o, ms, op, L)
-               : dispatch_subw<VEC, EPI_RELU, false>(subw, o, ms, op, L);
-  return add ? dispatch_subw<VEC, EPI_NONE, true>(subw, o, ms, op, L)
-             : dispatch_subw<VEC, EPI_NONE, false>(subw, o, ms, op, L);
-}
 
 // ---- COLTILE plan: header {magic, n_chunks} | padded offsets | counts | chunk_ptr | CUB temp |
 // packed entries (int2, 16-byte aligned). See coltile.cuh.
@@ -153,8 +68,9 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
   if (ldb < k || ldc < k || (D && ldd < k)) return fail(STC_EINVAL, "leading dimension smaller than k");
   if (epilogue != STC_EPILOGUE_NONE && epilogue != STC_EPILOGUE_RELU)
     return fail(STC_EINVAL, "unknown epilogue %d", epilogue);
-  if ((long long)(n + 1) * ldb >= (1LL << 32))
-    return fail(STC_EUNSUPPORTED, "dense operand of 2^32 elements or more (32-bit gather offsets)");
+  // dense operands of 2^32 elements or more gather with 64-bit addresses (spmm_wide.cu)
+  // (batched: B advances per batch in 64 bits, offsets are within one batch's operand)
+  const bool wide = (long long)(n + 1) * ldb >= (1LL << 32);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec4 = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C) &&
                     (!D || (ldd % 4 == 0 && aligned16(D))) && (val_bs % 4 == 0 || batch == 1) &&
@@ -197,6 +113,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
     ms.counters = reinterpret_cast<int*>(ms.tail_buf + (long long)batch * slabs * n_cta * sw);
   }
   Launch L{variant, batch, st, B, (size_t)((long long)n * ldb * (batch > 1 && b_bs ? batch : 1)) * sizeof(float)};
+  if (wide) return spmm_wide(vec4 ? 4 : 1, epilogue, D != nullptr, o, ms, colidx, vals, B, ldb, L);
   if (vec4) {
     SpmmOp<4> op{colidx, vals, B, ldb};
     return dispatch_spmm<4>(epilogue, D != nullptr, o, ms, op, L);
@@ -424,8 +341,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   if (variant != STC_VARIANT_ROW && variant != STC_VARIANT_MERGE)
     return fail(STC_EUNSUPPORTED, "MTTKRP supports ROW and MERGE");
   if (n_j < 0 || n_k < 0) return fail(STC_EINVAL, "negative factor extent");
-  if ((long long)(n_j + 1) * ldb >= (1LL << 32) || (long long)(n_k + 1) * ldcf >= (1LL << 32))
-    return fail(STC_EUNSUPPORTED, "factor matrix of 2^32 elements or more (32-bit gather offsets)");
+  const bool wide = (long long)(n_j + 1) * ldb >= (1LL << 32) || (long long)(n_k + 1) * ldcf >= (1LL << 32);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec4 = rank % 4 == 0 && ldb % 4 == 0 && ldcf % 4 == 0 && ldm % 4 == 0 && aligned16(B) &&
                     aligned16(C) && aligned16(M);
@@ -448,6 +364,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
     ms.counters = reinterpret_cast<int*>(ms.tail_buf + ceil_div(rank, sw) * n_cta * sw);
   }
   Launch L{variant, 1, st, B, (size_t)((long long)n_j * ldb) * sizeof(float)};
+  if (wide) return mttkrp_wide(vec, o, ms, jcrd, kcrd, vals, B, ldb, C, ldcf, subw, L);
   if (vec4) {
     MttkrpOp<4> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
     return dispatch_subw<4, EPI_NONE, false>(subw, o, ms, op, L);

@@ -233,3 +233,74 @@ def test_tiled_attention_matches_oracle(seq, window, nrand, heads):
         ob = native.spmm_csr(M.rowptr, M.colidx, p, np.abs(V[h]))
         ok, worst = parity_gate(O[h], o, ob, TOL)
         assert ok, worst
+
+
+# ---- dense operands of 2^32 elements or more (64-bit gathers, spmm_wide.cu) -------------------------
+
+def _wide_operand(n, k, used, rng):
+    """An (n, k) fp32 device operand (> 2^32 elements, ~17 GB) whose rows in `used` hold
+    seeded values; the other rows are never read. Returns (B, compact host copy, remap)."""
+    B = torch.empty((n, k), dtype=torch.float32, device="cuda")
+    used = np.unique(used)
+    vals = rng.uniform(-1, 1, (len(used), k)).astype(np.float32)
+    B[torch.from_numpy(used).cuda().long()] = torch.from_numpy(vals).cuda()
+    remap = np.full(n, -1, dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    return B, vals, remap
+
+
+@pytest.mark.parametrize("variant", ["row", "merge"])
+def test_spmm_dense_operand_beyond_32bit_offsets(variant):
+    rng = np.random.default_rng(77)
+    k = 128
+    n = (1 << 32) // k + 4099                     # (n + 1) * k > 2^32: 64-bit gathers
+    m = 700
+    # rows: ~half their columns near the start, the rest past the 32-bit offset boundary
+    rows = []
+    for L in np.where(np.arange(m) % 50 == 7, 900, rng.integers(0, 24, m)):
+        c = np.unique(np.concatenate([rng.integers(0, 1000, L // 2 + 1), rng.integers(n - 200_000, n, L)]))[:L]
+        rows.append(np.sort(c))
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in rows], out=rp[1:])
+    ci = np.concatenate(rows).astype(np.int64)
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    try:
+        B, host_rows, remap = _wide_operand(n, k, ci, rng)
+    except torch.OutOfMemoryError:
+        pytest.skip("device too small for a 2^32-element operand")
+    R, C, V = dev(rp, ci, v)
+    got = ops.spmm_csr(R, C, V, B, relu=True, variant=variant).cpu().numpy()
+    want = native.spmm_csr(rp, remap[ci], v, host_rows, relu=True)
+    bound = native.spmm_csr(rp, remap[ci], np.abs(v), np.abs(host_rows))
+    assert parity_gate(got, want, bound, TOL)[0]
+    del B
+    torch.cuda.empty_cache()
+
+
+def test_mttkrp_factor_beyond_32bit_offsets():
+    rng = np.random.default_rng(78)
+    R = 32
+    nj = (1 << 32) // R + 777                    # B has more than 2^32 elements
+    dim_i, dim_k = 200, 300
+    i = np.sort(rng.integers(0, dim_i, 4000))
+    j = np.where(rng.random(4000) < 0.5, rng.integers(0, 500, 4000), rng.integers(nj - 5000, nj, 4000))
+    k = rng.integers(0, dim_k, 4000)
+    key = np.unique(np.stack([i, j, k], 1), axis=0)
+    i, j, k = key[:, 0], key[:, 1], key[:, 2]
+    vals = rng.uniform(0, 1, len(i)).astype(np.float32)
+    try:
+        B, host_b, remap = _wide_operand(nj, R, j, rng)
+    except torch.OutOfMemoryError:
+        pytest.skip("device too small for a 2^32-element operand")
+    Cf = rng.uniform(0, 1, (dim_k, R)).astype(np.float32)
+    seg = ops.coo_segments(torch.from_numpy(i).int().cuda())
+    _, ptr_ref = restate.coo_segments(i)
+    Jt, Kt = torch.from_numpy(j).int().cuda(), torch.from_numpy(k).int().cuda()
+    Vt = torch.from_numpy(vals).cuda()
+    want = native.mttkrp(ptr_ref, remap[j], k, vals, host_b, Cf)
+    bound = native.mttkrp(ptr_ref, remap[j], k, np.abs(vals), np.abs(host_b), np.abs(Cf))
+    for variant in ("row", "merge"):
+        got = ops.mttkrp_coo3(seg, Jt, Kt, Vt, B, torch.from_numpy(Cf).cuda(), variant=variant).cpu().numpy()
+        assert parity_gate(got, want, bound, TOL)[0]
+    del B
+    torch.cuda.empty_cache()
