@@ -22,8 +22,9 @@ operand), so the iteration space is exactly the reference's:
 * a loop with no sparse participant expands by its full extent;
 * the keys a term visits are snapshotted after its deepest output loop, so a key
   whose inner reduction is empty is still stored (value 0.0), as in the reference;
-* products and sums run in float64 on the device, the result is rounded once to
-  float32 (storage dtype), and the output is assembled by ``tensor._assemble_sorted``
+* products and sums run in float64 on the device — per-key sums by a stable sort and a
+  segmented reduction, no atomics, so results are bit-reproducible — the result is
+  rounded once to float32 (storage dtype), and the output is assembled by ``tensor._assemble_sorted``
   (the device restatement of `_assemble_presorted`, `tensor.py:162-219`).
 
 Operands stored in an order that violates the loop order are converted first
@@ -310,21 +311,20 @@ def execute_generic(sched: Schedule, tensor_of: dict, out_fmt: TensorFormat, cou
         all_rows.append(row_key)
         all_prod.append(prod)
     size = math.prod(ext[v] for v in out_chain)
+    # per-key sums in a fixed order (stable sort by key, terms in expression order, then a
+    # segmented reduction): no floating-point atomics, bit-reproducible run to run
+    ukeys, sums = _segment_sums(torch.cat(all_rows), torch.cat(all_prod))
     if not out_fmt.has_sparse_levels:
         flat = torch.zeros(size, dtype=torch.float64, device=dev)
-        for rk, pr in zip(all_rows, all_prod):
-            flat.index_add_(0, rk, pr)
-        counter.add(0, sum(int(r.numel()) for r in all_rows), 0)
+        flat[ukeys] = sums
         st = TensorStorage(out_fmt, tuple(DenseLevel(out_fmt.level_extent(k)) for k in range(out_fmt.order)),
                            flat.to(VALUE_DTYPE))
         st.validate()
         return Tensor(e.output_name, shape, st)
-    keys = torch.unique(torch.cat(all_keys)) if all_keys else torch.zeros(0, dtype=torch.long, device=dev)
+    keys = torch.unique(torch.cat(all_keys))
     vals = torch.zeros(keys.numel(), dtype=torch.float64, device=dev)
-    for rk, pr in zip(all_rows, all_prod):
-        if rk.numel():
-            vals.index_add_(0, torch.searchsorted(keys, rk), pr)
-    counter.add(0, sum(int(r.numel()) for r in all_rows), 0)
+    if ukeys.numel():
+        vals[torch.searchsorted(keys, ukeys)] = sums
     perm_cols = torch.empty((keys.numel(), len(out_chain)), dtype=torch.long, device=dev)
     rem = keys.clone()
     for k in reversed(range(len(out_chain))):
@@ -332,3 +332,13 @@ def execute_generic(sched: Schedule, tensor_of: dict, out_fmt: TensorFormat, cou
         perm_cols[:, k] = rem % e_k
         rem = rem // e_k
     return _assemble_sorted(shape, out_fmt, perm_cols, vals.to(VALUE_DTYPE), e.output_name)
+
+
+def _segment_sums(row_key: torch.Tensor, prod: torch.Tensor):
+    """(distinct keys ascending, float64 sum of each key's products in input order)."""
+    if not row_key.numel():
+        return row_key, prod
+    order = torch.argsort(row_key, stable=True)
+    sk, sv = row_key[order], prod[order]
+    ukeys, counts = torch.unique_consecutive(sk, return_counts=True)
+    return ukeys, torch.segment_reduce(sv, "sum", lengths=counts)
