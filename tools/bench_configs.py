@@ -224,12 +224,42 @@ def ewise_cfg1():
                   {"nnz_out": nnz_c})
 
 
+def walker_ttv_cfg5():
+    """Device loop-nest walker (no dedicated kernel) at scale: tensor-times-vector
+    y(i,j) = T(i,j,k) * x(k) on the cfg5 tensor (6.55 M entries), through the public API."""
+    import paper_2405_16883_b200 as st
+
+    (i, j, k), vals, _, _ = synthetic.cfg5()
+    dim = 20000
+    T = st.coo_from_sorted_arrays((i, j, k), vals, (dim, dim, dim), name="T")
+    xv = np.random.default_rng(3).uniform(0, 1, dim).astype(np.float32)
+    x = st.from_dense(torch.from_numpy(xv).cuda(), name="x")
+    e = st.parse("y(i,j) = T(i,j,k) * x(k)", {"T": T, "x": x})
+    out, _, rep = st.run_with_report(e)
+    assert rep["variants"][0].startswith("generic:device-walk"), rep["variants"]
+    # parity: float64 fiber sums on the host, structure = the distinct (i, j) fibers
+    first = np.ones(len(i), bool)
+    first[1:] = (i[1:] != i[:-1]) | (j[1:] != j[:-1])
+    starts = np.flatnonzero(first)
+    want = np.add.reduceat(vals.astype(np.float64) * xv[k].astype(np.float64), starts)
+    got = out.storage.values.cpu().numpy().astype(np.float64)
+    assert got.shape == want.shape and np.allclose(got, want, rtol=1e-6, atol=1e-9)
+    ms = gpu_time(lambda: st.run(e), reps=5)
+    nbytes = 16.0 * len(vals) + 4 * dim + 8 * len(starts)
+    v64, x64 = vals.astype(np.float64), xv.astype(np.float64)
+    cs = cpu_time(lambda: np.add.reduceat(v64 * x64[k], starts), 2.0)
+    return record("x3_walker_ttv_cfg5", ms, 2.0 * len(vals), nbytes, "hbm", cs, "numpy fiber sums (1 thread)",
+                  {"nnz": int(len(vals)), "fibers": int(len(starts)), "out_format": out.format.name(),
+                   "path": rep["variants"][0][:40]})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--configs", default="1,2,3,4,5,x1,x2")
+    ap.add_argument("--configs", default="1,2,3,4,5,x1,x2,x3")
     a = ap.parse_args()
-    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "x1": spgemm_cfg1, "x2": ewise_cfg1}
+    fns = {"1": cfg1, "2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5, "x1": spgemm_cfg1, "x2": ewise_cfg1,
+           "x3": walker_ttv_cfg5}
     res = [fns[c]() for c in a.configs.split(",")]
     if a.out:
         Path(a.out).write_text(json.dumps({"device": PROPS.name, "sms": PROPS.multi_processor_count,
