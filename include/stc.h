@@ -71,8 +71,9 @@ int stc_l2_reset_persisting(void);
 
 /* Merge-path partition of a compressed row structure (plan time).
  * Groups own `items_per_group` consecutive items of the merged sequence
- * (m row ends + nnz entries). Writes (row, pos) int pairs for groups
- * 0..n_groups into `starts` (2*(n_groups+1) ints).                           */
+ * (m row ends + nnz entries, one item each).
+ * Writes (row, pos) int pairs for groups 0..n_groups into `starts`
+ * (2*(n_groups+1) ints).                                                     */
 long long stc_merge_path_groups(int m, long long nnz, int items_per_group);
 int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
                              int* starts, void* stream);

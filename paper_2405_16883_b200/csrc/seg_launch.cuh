@@ -18,7 +18,7 @@ inline int choose_subw(int k, int vec) {
   return 32;
 }
 
-inline long long n_groups_for(int m, long long nnz, int ipg) { return ceil_div((long long)m + nnz, ipg); }
+inline long long n_groups_for(int m, long long nnz, int ipg) { return ceil_div(merge_total_items(m, nnz), ipg); }
 
 inline size_t merge_ws_bytes(int m, long long nnz, int k, int subw, int vec, int ipg, int batch) {
   const long long groups = n_groups_for(m, nnz, ipg);

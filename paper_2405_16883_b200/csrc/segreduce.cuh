@@ -29,6 +29,16 @@
 
 namespace stc {
 
+#ifdef STC_DBG_TIMING
+// Diagnostic build only (tools/merge_balance_probe.py): per-group globaltimer stamps.
+__device__ unsigned long long g_dbg[1 << 16][4];
+STC_DEVICE unsigned long long dbg_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // Gather ops
 // ---------------------------------------------------------------------------
@@ -49,7 +59,9 @@ struct SpmmOp {
   static constexpr int kRing = 8;           // gathers in flight per group
   static constexpr int kMinBlocks = 4;      // resident CTAs per SM (register budget)
   static constexpr int kStageUnroll = 8;    // item loads per lane in flight while staging
-  static constexpr int kStageBytes = 32768;  // staged items per CTA (rest of SMEM stays L1)
+  // staged items per CTA; the rest of SMEM stays L1, which the in-flight gathers need
+  // (36 KB: 129 us on cfg2 against 100 us at 32 KB)
+  static constexpr int kStageBytes = 32768;
   struct Item {
     unsigned off;
     float v;
@@ -214,25 +226,46 @@ STC_DEVICE void write_row(const SegOut& o, int row, int col0, Frag<VEC> acc) {
 
 // ---------------------------------------------------------------------------
 // Plan-time merge-path partition: starts[g] = (row, pos) at diagonal g*IPG.
+//
+// The merged sequence weighs a row end kRowCost items and an entry one item. Item
+// positions: entry q of row r starts at q + kRowCost*r, the end of row r at
+// rowptr[r+1] + kRowCost*r; a group owns the items that start inside its range.
+// A row end costs about two gathers (per-group globaltimer stamps on cfg2: 0.147 us
+// per entry + 0.282 us per row end, tools/merge_balance_probe.py), and kRowCost = 2
+// narrows the finish-time spread (p10-p90 71.7-90.9 us -> 78.8-86.6 us), but the
+// larger item count per group (547 > the 512-item staging window) costs a second
+// synchronous staging round trip for most groups: 100.4 -> 104.5 us. Kept at 1.
 // ---------------------------------------------------------------------------
+
+constexpr int kRowCost = 1;
+
+__host__ __device__ inline long long merge_total_items(int m, long long nnz) {
+  return (long long)kRowCost * m + nnz;
+}
 
 static __global__ void merge_partition_kernel(int m, long long nnz, const int* __restrict__ rowptr,
                                               int ipg, int n_groups, int2* __restrict__ starts) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g > n_groups) return;
-  const long long total = (long long)m + nnz;
+  const long long total = merge_total_items(m, nnz);
   long long diag = (long long)g * ipg;
   if (diag > total) diag = total;
-  // largest t in [0, m] with t == 0 || rowptr[t] + t <= diag  (monotone in t)
+  // t = row ends starting before diag: largest t in [0, m] with t == 0 ||
+  // rowptr[t] + kRowCost*(t-1) < diag (monotone in t)
   int lo = 0, hi = m;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if ((long long)rowptr[mid] + mid <= diag)
+    if ((long long)rowptr[mid] + (long long)kRowCost * (mid - 1) < diag)
       lo = mid;
     else
       hi = mid - 1;
   }
-  starts[g] = make_int2(lo, (int)(diag - lo));
+  // entries of row t starting before diag
+  long long p = diag - (long long)kRowCost * lo;
+  const long long p_lo = rowptr[lo];
+  const long long p_hi = lo < m ? (long long)rowptr[lo + 1] : nnz;
+  p = p < p_lo ? p_lo : (p > p_hi ? p_hi : p);
+  starts[g] = make_int2(lo, (int)p);
 }
 
 // ---------------------------------------------------------------------------
@@ -341,6 +374,9 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   const int row0 = s.x;
   const int n_rows = e.x - s.x;   // rows whose end item this group owns
   const int n_nnz = e.y - s.y;    // entries this group accumulates
+#ifdef STC_DBG_TIMING
+  const unsigned long long t_start = dbg_timer();
+#endif
 
   // row ends of rows [row0 + rb, row0 + rb + CAPR), relative to s.y
   int rb = 0;
@@ -440,6 +476,14 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     if (col_ok) acc.store_plain(&Ts[sub * SW + lane * VEC]);
     if (lane == 0) Trow[sub] = row0 + r;
   }
+#ifdef STC_DBG_TIMING
+  if (lane == 0 && g < (1 << 16) && blockIdx.y == 0 && blockIdx.z == 0) {
+    g_dbg[g][0] = t_start;
+    g_dbg[g][1] = dbg_timer();
+    g_dbg[g][2] = (unsigned long long)n_rows;
+    g_dbg[g][3] = ((unsigned long long)n_nnz << 32) | (unsigned)(threadIdx.x / 32 + (blockIdx.x << 8));
+  }
+#endif
   __syncthreads();
 
   // ---- CTA-level combine (position order: tails of earlier groups, then head) ----
@@ -502,7 +546,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     n_fix = 0;
     const long long ci = (long long)NG * ms.ipg;
     auto arrive = [&](int r, int c_last) {
-      const int c_first = (int)(((long long)o.rowptr[r] + r) / ci);
+      const int c_first = (int)(((long long)o.rowptr[r] + (long long)kRowCost * r) / ci);
       const int need = c_last - c_first + 1;
       int* ctr = ms.counters + zslab + c_last;
       if (atomicAdd(ctr, 1) + 1 == need) {
@@ -516,7 +560,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     if (head_row_s >= 0) arrive(head_row_s, cta);
     if (tail_row_s >= 0) {
       const int r = tail_row_s;
-      arrive(r, (int)(((long long)o.rowptr[r + 1] + r) / ci));
+      arrive(r, (int)(((long long)o.rowptr[r + 1] + (long long)kRowCost * r) / ci));
     }
     __threadfence();
   }

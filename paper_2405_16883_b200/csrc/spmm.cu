@@ -139,7 +139,7 @@ int plan_ipg(int m, long long nnz, int k, int batch) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   const long long slabs = ceil_div(k, SUBW * VEC);
-  const long long total = (long long)m + nnz;
+  const long long total = merge_total_items(m, nnz);
   const long long cta_slots = (long long)sms * per_sm;
   // CTAs available per (slab, batch) in one wave
   long long ctas = cta_slots / (slabs * batch);
@@ -372,3 +372,10 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   MttkrpOp<1> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
   return dispatch_subw<1, EPI_NONE, false>(subw, o, ms, op, L);
 }
+
+#ifdef STC_DBG_TIMING
+// Diagnostic build only: copy the per-group timing stamps of the last merge launch.
+extern "C" int stc_debug_timing(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, stc::g_dbg, bytes);
+}
+#endif

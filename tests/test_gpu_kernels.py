@@ -90,11 +90,17 @@ def test_merge_partition_matches_host_search():
         part = ops.merge_partition(R, len(v), ipg)
         st = part.starts.cpu().numpy().reshape(-1, 2)
         m, nnz = 500, len(v)
-        diags = np.minimum(np.arange(part.n_groups + 1) * ipg, m + nnz)
-        key = rp[1:] + np.arange(1, m + 1)
-        rows = np.searchsorted(key, diags, side="right")
+        # items: an entry weighs 1, a row end W (segreduce.cuh kRowCost); a group owns the
+        # items that start in [g*ipg, (g+1)*ipg): entry q of row r starts at q + W*r, the
+        # end of row r at rp[r+1] + W*r
+        W = 1
+        diags = np.minimum(np.arange(part.n_groups + 1) * ipg, W * m + nnz)
+        end_starts = rp[1:] + W * np.arange(m)
+        rows = np.searchsorted(end_starts, diags, side="left")     # row ends starting before diag
+        pos = np.clip(diags - W * rows, rp[rows], rp[np.minimum(rows + 1, m)])
+        assert part.n_groups == -(-(W * m + nnz) // ipg)
         assert np.array_equal(st[:, 0], rows)
-        assert np.array_equal(st[:, 1], diags - rows)
+        assert np.array_equal(st[:, 1], pos)
 
 
 def test_spmm_deterministic_bitwise():
