@@ -56,3 +56,11 @@ cta = (d[:, 3] & np.uint64(0xffffff)).astype(np.int64) >> 8
 cta_end = np.zeros(cta.max() + 1)
 np.maximum.at(cta_end, cta, end)
 print("CTA finish: p10 %.1f p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(cta_end, [10, 50, 90, 100])))
+slow = np.argsort(-end)[:12]
+print("slowest groups (g, cta, rows, nnz, start us, end us):")
+for gi in slow:
+    print(f"  {gi:5d} {cta[gi]:4d} {rows[gi]:4d} {nnz[gi]:4d} {start[gi]:6.1f} {end[gi]:6.1f}")
+fast = np.argsort(end)[:5]
+print("fastest groups:")
+for gi in fast:
+    print(f"  {gi:5d} {cta[gi]:4d} {rows[gi]:4d} {nnz[gi]:4d} {start[gi]:6.1f} {end[gi]:6.1f}")
