@@ -25,11 +25,11 @@ def _dense(rng, shape, name):
     return st.from_dense(rng.uniform(-1, 1, shape).astype(np.float32).astype(np.float64), name=name)
 
 
-def _hot_path_case(rng):
+def _hot_path_case(rng, cap=40):
     names = list("ijklmnpq")
     rng.shuffle(names)
     i, j, k = names[:3]
-    m, n, K = (int(x) for x in rng.integers(1, 40, 3))
+    m, n, K = (int(x) for x in rng.integers(1, cap, 3))
     dens = float(rng.choice([0.05, 0.2, 0.5]))
     kind = rng.choice(["spmm", "spmv", "spmm_add", "spmm_bt", "sddmm", "mttkrp", "spgemm", "add", "mul"])
     if kind in ("spmm", "spmm_add", "spmm_bt", "spmv"):
