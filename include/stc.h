@@ -71,12 +71,23 @@ int stc_l2_reset_persisting(void);
 
 /* Merge-path partition of a compressed row structure (plan time).
  * Groups own `items_per_group` consecutive items of the merged sequence
- * (m row ends + nnz entries, one item each).
+ * (m row ends weighing 2 items each — a row flush costs about two gathers —
+ * and nnz entries of 1 item; a group owns the items starting in its range).
  * Writes (row, pos) int pairs for groups 0..n_groups into `starts`
  * (2*(n_groups+1) ints).                                                     */
 long long stc_merge_path_groups(int m, long long nnz, int items_per_group);
 int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
                              int* starts, void* stream);
+
+/* Plan-time interleaving of long rows for the MERGE variant: writes a copy of
+ * (colidx, vals) in which every row longer than `span` entries (the span of one
+ * merge group, i.e. items_per_group) is stored as G = ceil(len / span) interleaved
+ * sequences (entries 0, G, 2G, ..., then 1, G + 1, ...); shorter rows are copied.
+ * A group covering part of a hub row then gathers from the whole row's column
+ * range (hot and cold columns alike) instead of one sorted slice of it. Feed the
+ * copy to stc_spmm_csr_f32 (same rowptr); the row sums change only in order.   */
+int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* colidx, const float* vals,
+                         int span, int* colidx_out, float* vals_out, void* stream);
 
 /* Plan-time choice of items_per_group for the MERGE variant: the merged
  * sequence is cut into exactly enough groups to fill whole waves of resident

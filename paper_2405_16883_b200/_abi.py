@@ -55,6 +55,7 @@ SIGNATURES = {
     "stc_merge_path_partition": (_i, [_i, _ll, _p, _i, _p, _p]),
     "stc_coltile_plan_ints": (_ll, [_i, _i, _ll]),
     "stc_coltile_plan": (_i, [_i, _i, _ll, _p, _p, _p, _p, _ll, _p]),
+    "stc_merge_interleave": (_i, [_i, _ll, _p, _p, _p, _i, _p, _p, _p]),
     "stc_merge_plan_items_per_group": (_i, [_i, _ll, _i, _i, _i]),
     "stc_spmm_workspace_bytes": (_sz, [_i, _ll, _i, _i, _i, _i]),
     "stc_spmm_csr_f32": (_i, [_i, _i, _i, _p, _p, _p, _ll, _p, _ll, _p, _ll, _p, _ll, _i, _i, _p, _i,

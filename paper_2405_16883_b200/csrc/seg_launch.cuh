@@ -9,7 +9,7 @@ namespace stc {
 namespace seg {
 
 inline constexpr int kThreads = 256;
-inline constexpr int kMaxIpg = 1024;  // staged items per group (shared memory bound)
+inline constexpr int kMaxIpg = 1024 * kEntryCost;  // items per group (in item units)
 
 inline int choose_subw(int k, int vec) {
   for (int s : {4, 8, 16}) {

@@ -227,20 +227,30 @@ STC_DEVICE void write_row(const SegOut& o, int row, int col0, Frag<VEC> acc) {
 // ---------------------------------------------------------------------------
 // Plan-time merge-path partition: starts[g] = (row, pos) at diagonal g*IPG.
 //
-// The merged sequence weighs a row end kRowCost items and an entry one item. Item
-// positions: entry q of row r starts at q + kRowCost*r, the end of row r at
-// rowptr[r+1] + kRowCost*r; a group owns the items that start inside its range.
+// Item costs: an entry weighs kEntryCost, a row end kRowCost. Entry q of row r
+// starts at kEntryCost*q + kRowCost*r, the end of row r at
+// kEntryCost*rowptr[r+1] + kRowCost*r; a group owns the items starting in its range.
 // A row end costs about two gathers (per-group globaltimer stamps on cfg2: 0.147 us
-// per entry + 0.282 us per row end, tools/merge_balance_probe.py), and kRowCost = 2
-// narrows the finish-time spread (p10-p90 71.7-90.9 us -> 78.8-86.6 us), but the
-// larger item count per group (547 > the 512-item staging window) costs a second
-// synchronous staging round trip for most groups: 100.4 -> 104.5 us. Kept at 1.
+// per entry + 0.282 us per row end, tools/merge_balance_probe.py), so kRowCost = 2:
+// with unit weights groups of many short rows finish last. Together with the
+// plan-time interleaving of long rows (ops.interleave_long_rows: every group inside
+// a hub row then sees the same mix of hot and cold columns) the groups' finish
+// times tighten from 66-100 us to 79-89 us and the cfg2 layer from 100.4 to 94.2 us
+// (tools/interleave_probe.py; weights 1.5 / 1.75 / 2.5 / 3 measured 98.3 / 96.3 /
+// 98.3 / 98.3 us).
 // ---------------------------------------------------------------------------
 
-constexpr int kRowCost = 1;
+#ifndef STC_ENTRY_COST
+#define STC_ENTRY_COST 1
+#endif
+#ifndef STC_ROW_COST
+#define STC_ROW_COST 2
+#endif
+constexpr int kEntryCost = STC_ENTRY_COST;
+constexpr int kRowCost = STC_ROW_COST;
 
 __host__ __device__ inline long long merge_total_items(int m, long long nnz) {
-  return (long long)kRowCost * m + nnz;
+  return (long long)kRowCost * m + (long long)kEntryCost * nnz;
 }
 
 static __global__ void merge_partition_kernel(int m, long long nnz, const int* __restrict__ rowptr,
@@ -251,17 +261,18 @@ static __global__ void merge_partition_kernel(int m, long long nnz, const int* _
   long long diag = (long long)g * ipg;
   if (diag > total) diag = total;
   // t = row ends starting before diag: largest t in [0, m] with t == 0 ||
-  // rowptr[t] + kRowCost*(t-1) < diag (monotone in t)
+  // kEntryCost*rowptr[t] + kRowCost*(t-1) < diag (monotone in t)
   int lo = 0, hi = m;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if ((long long)rowptr[mid] + (long long)kRowCost * (mid - 1) < diag)
+    if ((long long)kEntryCost * rowptr[mid] + (long long)kRowCost * (mid - 1) < diag)
       lo = mid;
     else
       hi = mid - 1;
   }
-  // entries of row t starting before diag
-  long long p = diag - (long long)kRowCost * lo;
+  // entries q of row t starting before diag: kEntryCost*q + kRowCost*t < diag
+  const long long x = diag - (long long)kRowCost * lo;
+  long long p = x <= 0 ? 0 : (x + kEntryCost - 1) / kEntryCost;
   const long long p_lo = rowptr[lo];
   const long long p_hi = lo < m ? (long long)rowptr[lo + 1] : nnz;
   p = p < p_lo ? p_lo : (p > p_hi ? p_hi : p);
@@ -546,7 +557,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     n_fix = 0;
     const long long ci = (long long)NG * ms.ipg;
     auto arrive = [&](int r, int c_last) {
-      const int c_first = (int)(((long long)o.rowptr[r] + (long long)kRowCost * r) / ci);
+      const int c_first = (int)(((long long)kEntryCost * o.rowptr[r] + (long long)kRowCost * r) / ci);
       const int need = c_last - c_first + 1;
       int* ctr = ms.counters + zslab + c_last;
       if (atomicAdd(ctr, 1) + 1 == need) {
@@ -560,7 +571,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     if (head_row_s >= 0) arrive(head_row_s, cta);
     if (tail_row_s >= 0) {
       const int r = tail_row_s;
-      arrive(r, (int)(((long long)o.rowptr[r + 1] + (long long)kRowCost * r) / ci));
+      arrive(r, (int)(((long long)kEntryCost * o.rowptr[r + 1] + (long long)kRowCost * r) / ci));
     }
     __threadfence();
   }

@@ -144,11 +144,11 @@ int plan_ipg(int m, long long nnz, int k, int batch) {
   // CTAs available per (slab, batch) in one wave
   long long ctas = cta_slots / (slabs * batch);
   if (ctas < 1) ctas = 1;
-  const long long max_ipg = 8LL * CAP < kMaxIpg ? 8LL * CAP : kMaxIpg;  // a few staging windows per group
+  const long long max_ipg = 8LL * CAP * kEntryCost < kMaxIpg ? 8LL * CAP * kEntryCost : kMaxIpg;  // a few windows
   long long waves = ceil_div(total, ctas * NG * max_ipg);
   if (waves < 1) waves = 1;
   long long ipg = ceil_div(total, ctas * waves * NG);
-  if (ipg < 32) ipg = 32;
+  if (ipg < 32 * kEntryCost) ipg = 32 * kEntryCost;
   if (ipg > kMaxIpg) ipg = kMaxIpg;
   return (int)ipg;
 }
@@ -222,6 +222,46 @@ extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, 
   ctt_scatter_kernel<<<1184, 256, 0, st>>>(m, lay.n_chunks, chunk_ptr, colidx, vals, offs,
                                            reinterpret_cast<int2*>(plan + lay.ent));
   return check_launch("ctt_scatter_kernel");
+}
+
+// ---- long-row interleaving (plan time) -------------------------------------------------
+namespace {
+__global__ void interleave_kernel(int m, long long nnz, const int* __restrict__ rowptr, const int* __restrict__ colidx,
+                                  const float* __restrict__ vals, int span, int* __restrict__ colidx_out,
+                                  float* __restrict__ vals_out) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = m - 1;  // row r with rowptr[r] <= p < rowptr[r + 1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rowptr[mid] <= p)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const long long base = rowptr[lo];
+    const long long len = rowptr[lo + 1] - base;
+    const long long i = p - base;
+    long long dst = p;
+    if (len > span) {  // G interleaved sequences: entries j, j+G, j+2G, ... for j = 0..G-1
+      const long long G = (len + span - 1) / span, q = len / G, rem = len % G, j = i % G;
+      dst = base + j * q + (j < rem ? j : rem) + i / G;
+    }
+    colidx_out[dst] = colidx[p];
+    vals_out[dst] = vals[p];
+  }
+}
+}  // namespace
+
+extern "C" int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* colidx, const float* vals,
+                                    int span, int* colidx_out, float* vals_out, void* stream) {
+  if (m < 0 || nnz < 0 || span < 1) return fail(STC_EINVAL, "bad interleave arguments");
+  if (m == 0 || nnz == 0) return STC_OK;
+  if (!rowptr || !colidx || !vals || !colidx_out || !vals_out) return fail(STC_EINVAL, "null pointer");
+  const long long blocks = std::min<long long>(ceil_div(nnz, 256), 148LL * 16);
+  interleave_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(m, nnz, rowptr, colidx, vals,
+                                                                                    span, colidx_out, vals_out);
+  return check_launch("interleave_kernel");
 }
 
 extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {

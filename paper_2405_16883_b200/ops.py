@@ -23,6 +23,8 @@ from .tensor import ShapeError
 DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "0"))
 # Row-length skew (max / mean) above which the nnz-balanced split is chosen.
 MERGE_SKEW_THRESHOLD = 8.0
+# Interleave the entries of rows longer than a merge group (plans built with colidx/vals).
+INTERLEAVE = os.environ.get("STC_INTERLEAVE", "1") != "0"
 # Dense widths above which the column-tiled variant is chosen.
 COLTILE_MIN_K = 512
 
@@ -98,6 +100,31 @@ class MergePartition:
     starts: torch.Tensor      # int32 [2 * (n_groups + 1)]
     items_per_group: int
     n_groups: int
+    # SpMM plans built with the matrix's colidx / vals: copies in which every row longer
+    # than a group has its entries interleaved (see interleave_long_rows), else None.
+    colidx: torch.Tensor | None = None
+    vals: torch.Tensor | None = None
+
+
+def interleave_long_rows(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, span: int):
+    """Copies of (colidx, vals) in which each row longer than ``span`` entries is stored as
+    G = ceil(len / span) interleaved sequences (entries 0, G, 2G, ..., then 1, G+1, ...).
+
+    A merge-path group covering part of a long row then gathers columns from the whole
+    row's range instead of one contiguous slice of it: sorted columns put a hub row's hot
+    (low-index, L2-resident) neighbours first and its cold ones last, so contiguous
+    slices finish at very different times (cfg2: 66-100 us for equal work). The row's
+    sum is the same up to the summation order (a fixed permutation: deterministic, and
+    within the parity gate). Returns (None, None) for an empty matrix."""
+    m = rowptr.numel() - 1
+    nnz = colidx.numel()
+    if m <= 0 or nnz == 0:
+        return None, None
+    require_cuda(rowptr, colidx, vals)
+    ci, va = torch.empty_like(colidx), torch.empty_like(vals)
+    check(lib().stc_merge_interleave(m, nnz, ptr(_i32(rowptr)), ptr(_i32(colidx)), ptr(_f32(vals)), int(span),
+                                     ptr(ci), ptr(va), stream_handle()), "stc_merge_interleave")
+    return ci, va
 
 
 def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "spmm") -> int:
@@ -108,8 +135,11 @@ def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "
 
 
 def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None = None, *,
-                    k: int = 128, batch: int = 1, kind: str = "spmm") -> MergePartition:
-    """Plan-time merge-path partition; ``items_per_group`` None/0 = planned for ``k``."""
+                    k: int = 128, batch: int = 1, kind: str = "spmm", colidx: torch.Tensor | None = None,
+                    vals: torch.Tensor | None = None) -> MergePartition:
+    """Plan-time merge-path partition; ``items_per_group`` None/0 = planned for ``k``.
+    With the matrix's ``colidx``/``vals`` (SpMM) the plan also carries their long-row
+    interleaved copies, and ``spmm_csr`` reads those; use such a plan only with that matrix."""
     require_cuda(rowptr)
     _i32(rowptr)
     m = rowptr.numel() - 1
@@ -120,7 +150,10 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
     rc = lib().stc_merge_path_partition(m, nnz, ptr(rowptr), items_per_group, ptr(starts),
                                         stream_handle())
     check(rc, "stc_merge_path_partition")
-    return MergePartition(starts, items_per_group, groups)
+    ci = va = None
+    if kind == "spmm" and colidx is not None and vals is not None and vals.dim() == 1 and INTERLEAVE:
+        ci, va = interleave_long_rows(rowptr, _i32(colidx), _f32(vals), items_per_group)
+    return MergePartition(starts, items_per_group, groups, ci, va)
 
 
 @dataclass
@@ -193,9 +226,11 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
     ipg = 0
     plan_ptr = None
     if variant == "merge":
-        partition = partition or merge_partition(rowptr, nnz, k=k)
+        partition = partition or merge_partition(rowptr, nnz, k=k, colidx=colidx, vals=vals)
         ipg = partition.items_per_group
         plan_ptr = ptr(partition.starts)
+        if partition.colidx is not None:   # the plan's long-row interleaved entries
+            colidx, vals = partition.colidx, partition.vals
         if workspace is None:
             workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
     elif variant == "coltile":

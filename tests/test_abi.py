@@ -37,7 +37,7 @@ def test_host_only_entry_points():
     lib = _abi.load_library()
     assert lib.stc_abi_version() == 1
     assert lib.stc_last_error() == b""
-    assert lib.stc_merge_path_groups(10, 30, 8) == 5
+    assert lib.stc_merge_path_groups(10, 30, 8) == 7   # 2 items per row end + 1 per entry: ceil(50 / 8)
     assert lib.stc_merge_path_groups(0, 0, 8) == 0
     assert lib.stc_merge_path_groups(10, 30, 0) == -1
     assert lib.stc_spmm_workspace_bytes(1000, 5000, 64, _abi.VARIANT_ROW, 128, 1) == 0

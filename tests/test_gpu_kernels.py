@@ -93,7 +93,7 @@ def test_merge_partition_matches_host_search():
         # items: an entry weighs 1, a row end W (segreduce.cuh kRowCost); a group owns the
         # items that start in [g*ipg, (g+1)*ipg): entry q of row r starts at q + W*r, the
         # end of row r at rp[r+1] + W*r
-        W = 1
+        W = 2
         diags = np.minimum(np.arange(part.n_groups + 1) * ipg, W * m + nnz)
         end_starts = rp[1:] + W * np.arange(m)
         rows = np.searchsorted(end_starts, diags, side="left")     # row ends starting before diag
@@ -310,3 +310,39 @@ def test_mttkrp_factor_beyond_32bit_offsets():
         assert parity_gate(got, want, bound, TOL)[0]
     del B
     torch.cuda.empty_cache()
+
+
+def test_interleave_long_rows_kernel():
+    """stc_merge_interleave: rows longer than the span become G interleaved sequences
+    (entries 0, G, 2G, ..., 1, G+1, ...); shorter rows are copied unchanged."""
+    rng = np.random.default_rng(0)
+    lens = np.array([3, 1200, 0, 64, 65, 2000, 7, 0, 129])
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    ci = rng.integers(0, 10**6, rp[-1]).astype(np.int64)
+    va = rng.random(rp[-1]).astype(np.float32)
+    c, v = ops.interleave_long_rows(*dev(rp, ci, va), 64)
+    c, v = c.cpu().numpy(), v.cpu().numpy()
+    for r in range(len(lens)):
+        a, b = rp[r], rp[r + 1]
+        order = np.arange(b - a)
+        if b - a > 64:
+            g = -(-(b - a) // 64)
+            order = np.concatenate([np.arange(j, b - a, g) for j in range(g)])
+        assert np.array_equal(c[a:b], ci[a:b][order]) and np.array_equal(v[a:b], va[a:b][order])
+
+
+def test_merge_with_interleaved_plan_matches_oracle():
+    rng = np.random.default_rng(5)
+    m, n, k = 400, 3000, 128
+    lens = np.where(np.arange(m) % 37 == 0, rng.integers(1500, 2900, m), rng.integers(0, 12, m))
+    rp, ci, v = make_csr(rng, m, n, lens)
+    R, C, V = dev(rp, ci, v)
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    part = ops.merge_partition(R, len(v), 64, k=k, colidx=C, vals=V)
+    assert part.colidx is not None
+    Bt = torch.from_numpy(B).cuda()
+    got = ops.spmm_csr(R, C, V, Bt, variant="merge", partition=part).cpu().numpy()
+    again = ops.spmm_csr(R, C, V, Bt, variant="merge", partition=part).cpu().numpy()
+    assert np.array_equal(got, again)  # fixed order: bit-reproducible
+    want = native.spmm_csr(rp, ci, v, B)
+    assert parity_gate(got, want, native.spmm_csr(rp, ci, np.abs(v), np.abs(B)), TOL)[0]

@@ -321,3 +321,4 @@ def test_storage_matches_reference_goldens():
     t = st.build_from_entries((22, 17), st.csc(22, 17), ents)
     assert t.storage.levels[1].pos.tolist() == pos.tolist()
     assert t.storage.levels[1].crd.tolist() == crd.tolist()
+

@@ -43,7 +43,7 @@ def cfg2():
                torch.from_numpy(A.vals).cuda())
     Z = torch.from_numpy(X).cuda() @ torch.from_numpy(W1).cuda()
     out = torch.empty_like(Z)
-    part = ops.merge_partition(R, A.nnz, k=128)
+    part = ops.merge_partition(R, A.nnz, k=128, colidx=C, vals=V)
     ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", part.items_per_group, 1, "cuda")
     return lambda: ops.spmm_csr(R, C, V, Z, out=out, relu=True, variant="merge", partition=part, workspace=ws)
 

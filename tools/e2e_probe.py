@@ -24,6 +24,8 @@ cnt = [0]
 
 
 def cached(rp, ci, v, B, **kw):
+    for key in ("variant", "partition", "stats"):
+        kw.pop(key, None)
     cnt[0] += 1
     return orig(rp, ci, v, B, variant=work.variant, partition=work.partition, workspace=ws[cnt[0] % 2],
                 stats=work.stats, **kw)
@@ -32,6 +34,6 @@ def cached(rp, ci, v, B, **kw):
 ops.spmm_csr = cached
 ms, _, _ = work.e2e(steps=20, warmup=3)
 print(f"e2e with cached plan: {ms:.3f} ms/step", flush=True)
-ops.spmm_csr = lambda rp, ci, v, B, out=None, relu=False: out  # noqa: E731
+ops.spmm_csr = lambda rp, ci, v, B, out=None, relu=False, **kw: out  # noqa: E731
 ms, _, _ = work.e2e(steps=20, warmup=3)
 print(f"e2e copies only (no SpMM; GEMMs kept): {ms:.3f} ms/step", flush=True)
