@@ -226,29 +226,29 @@ extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, 
 
 // ---- long-row interleaving (plan time) -------------------------------------------------
 namespace {
-// one warp per row (no per-entry row search): lanes stride over the row's entries
 __global__ void interleave_kernel(int m, long long nnz, const int* __restrict__ rowptr, const int* __restrict__ colidx,
                                   const float* __restrict__ vals, int span, int* __restrict__ colidx_out,
                                   float* __restrict__ vals_out) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
-    const long long base = rowptr[r];
-    const long long len = rowptr[r + 1] - base;
-    if (len > span) {  // G interleaved sequences: entries j, j+G, j+2G, ... for j = 0..G-1
-      const long long G = (len + span - 1) / span, q = len / G, rem = len % G;
-      for (long long i = lane; i < len; i += 32) {
-        const long long j = i % G;
-        const long long dst = base + j * q + (j < rem ? j : rem) + i / G;
-        colidx_out[dst] = ld_stream(colidx + base + i);
-        vals_out[dst] = ld_stream(vals + base + i);
-      }
-    } else {
-      for (long long i = lane; i < len; i += 32) {
-        colidx_out[base + i] = ld_stream(colidx + base + i);
-        vals_out[base + i] = ld_stream(vals + base + i);
-      }
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
+       p += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = m - 1;  // row r with rowptr[r] <= p < rowptr[r + 1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rowptr[mid] <= p)
+        lo = mid;
+      else
+        hi = mid - 1;
     }
+    const long long base = rowptr[lo];
+    const long long len = rowptr[lo + 1] - base;
+    const long long i = p - base;
+    long long dst = p;
+    if (len > span) {  // G interleaved sequences: entries j, j+G, j+2G, ... for j = 0..G-1
+      const long long G = (len + span - 1) / span, q = len / G, rem = len % G, j = i % G;
+      dst = base + j * q + (j < rem ? j : rem) + i / G;
+    }
+    colidx_out[dst] = colidx[p];
+    vals_out[dst] = vals[p];
   }
 }
 }  // namespace
@@ -258,7 +258,7 @@ extern "C" int stc_merge_interleave(int m, long long nnz, const int* rowptr, con
   if (m < 0 || nnz < 0 || span < 1) return fail(STC_EINVAL, "bad interleave arguments");
   if (m == 0 || nnz == 0) return STC_OK;
   if (!rowptr || !colidx || !vals || !colidx_out || !vals_out) return fail(STC_EINVAL, "null pointer");
-  const long long blocks = std::min<long long>(ceil_div((long long)m * 32, 256), 148LL * 16);
+  const long long blocks = std::min<long long>(ceil_div(nnz, 256), 148LL * 16);
   interleave_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(m, nnz, rowptr, colidx, vals,
                                                                                     span, colidx_out, vals_out);
   return check_launch("interleave_kernel");
