@@ -239,13 +239,13 @@ __global__ void interleave_kernel(int m, long long nnz, const int* __restrict__ 
       else
         hi = mid - 1;
     }
-    const long long base = rowptr[lo];
-    const long long len = rowptr[lo + 1] - base;
-    const long long i = p - base;
+    const int base = rowptr[lo];
+    const int len = rowptr[lo + 1] - base;
+    const int i = (int)(p - base);
     long long dst = p;
     if (len > span) {  // G interleaved sequences: entries j, j+G, j+2G, ... for j = 0..G-1
-      const long long G = (len + span - 1) / span, q = len / G, rem = len % G, j = i % G;
-      dst = base + j * q + (j < rem ? j : rem) + i / G;
+      const int G = (len + span - 1) / span, q = len / G, rem = len % G, j = i % G;
+      dst = (long long)base + (long long)j * q + (j < rem ? j : rem) + i / G;
     }
     colidx_out[dst] = colidx[p];
     vals_out[dst] = vals[p];
