@@ -51,6 +51,7 @@ from .tensor import (
     TensorStorage,
     VALUE_DTYPE,
     _assemble,
+    convert,
     stored_entries_torch,
     to_torch,
 )
@@ -362,16 +363,19 @@ class _MttkrpTerm:
 
 
 def _match_mttkrp(term, out_vars) -> _MttkrpTerm | None:
+    """MTTKRP in any mode: M(i,r) = T(..i..) * B(j,r) * C(k,r), i one of T's indices
+    (CP-ALS runs all three modes). ``i`` is the output mode, ``j``/``k`` the other two
+    in T's index order."""
     if len(term) != 3 or len(out_vars) != 2:
         return None
     sp = [a for a in term if a.tensor.format.has_sparse_levels]
     if len(sp) != 1 or sp[0].tensor.order != 3:
         return None
     T = sp[0]
-    i, j, k = T.indices
-    if out_vars[0] != i:
+    i, r = out_vars
+    if i not in T.indices or r in T.indices:
         return None
-    r = out_vars[1]
+    j, k = (v for v in T.indices if v != i)
     dn = [a for a in term if a is not T]
     if any(a.tensor.format.has_sparse_levels or a.tensor.order != 2 for a in dn):
         return None
@@ -663,12 +667,20 @@ def _view_perm(t: Tensor, view: RowView) -> torch.Tensor:
 def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
     T = ctx.t(mk.T)
     f = T.format
-    if not (f.is_coordinate and f.mode_ordering == (0, 1, 2) and mk.T.indices == (mk.i, mk.j, mk.k)):
-        raise UnsupportedExpressionError("MTTKRP needs a COO tensor accessed in storage order")
-    if ctx.out_fmt.levels != (LevelFormat.COMPRESSED, LevelFormat.DENSE):
+    if not f.is_coordinate:
+        raise UnsupportedExpressionError("MTTKRP needs a COO tensor")
+    if ctx.out_fmt.levels != (LevelFormat.COMPRESSED, LevelFormat.DENSE) or ctx.out_fmt.mode_ordering != (0, 1):
         raise UnsupportedExpressionError("MTTKRP output must be [compressed, dense]")
-    st = T.storage
-    seg = _cache(T, ("coo_segments",), lambda: ops.coo_segments(st.levels[0].crd))
+    # the kernel walks entries sorted by (output mode, j, k): for another output mode (or
+    # another storage order) a device re-sorted COO view of T is built once and cached
+    order = tuple(mk.T.indices.index(v) for v in (mk.i, mk.j, mk.k))
+    view = T if f.mode_ordering == order else _cache(
+        T, ("mttkrp_view", order), lambda: convert(T, f.with_mode_ordering(order)))
+    st = view.storage
+    # op counters follow the reference, which walks T in its storage order for every mode
+    base = T.storage if f.mode_ordering == (0, 1, 2) else _cache(
+        T, ("mttkrp_view", (0, 1, 2)), lambda: convert(T, f.with_mode_ordering((0, 1, 2)))).storage
+    seg = _cache(view, ("coo_segments",), lambda: ops.coo_segments(st.levels[0].crd))
     Bd = _dense_torch(ctx.t(mk.B), (mk.B.indices.index(mk.j), mk.B.indices.index(mk.r)))
     Cd = _dense_torch(ctx.t(mk.C), (mk.C.indices.index(mk.k), mk.C.indices.index(mk.r)))
     if not mk.b_first:
@@ -677,7 +689,7 @@ def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
     else:
         jc, kc = st.levels[1].crd, st.levels[2].crd
     variant = ctx.variant if ctx.variant in ("row", "merge") else "merge"
-    part = _cache(T, ("partition", "mttkrp", Bd.shape[1]),
+    part = _cache(view, ("partition", "mttkrp", Bd.shape[1]),
                   lambda: ops.merge_partition(seg.ptr, st.values.numel(), k=Bd.shape[1], kind="mttkrp")) \
         if variant == "merge" else None
     M = ops.mttkrp_coo3(seg, jc, kc, st.values, Bd, Cd, variant=variant, partition=part)
@@ -686,18 +698,21 @@ def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
     R = Bd.shape[1]
     nblk = _n_blocks(R, ctx.sched, mk.r)
 
-    def distinct_ij():
-        c0, c1 = st.levels[0].crd, st.levels[1].crd
+    def distinct_prefix(levels):
+        c0 = base.levels[0].crd
         if nnz == 0:
             return 0
-        new = torch.ones(nnz, dtype=torch.bool, device=c0.device)
-        new[1:] = (c0[1:] != c0[:-1]) | (c1[1:] != c1[:-1])
+        new = torch.zeros(nnz, dtype=torch.bool, device=c0.device)
+        new[0] = True
+        for lv in base.levels[:levels]:
+            new[1:] |= lv.crd[1:] != lv.crd[:-1]
         return int(new.sum().item())
 
-    n_ij = _cache(T, ("distinct_ij",), distinct_ij)
-    body = 2 * seg.n_seg + 2 * n_ij + 2 * nnz
-    ctx.counter.add(2 * nnz * R, nnz * R, nblk * (1 + body) if nblk else body + seg.n_seg)
-    return _compressed_dense_result(ctx.expr.output_name, (T.shape[0], R), seg.rows, M)
+    n_i = seg.n_seg if base is st else _cache(T, ("distinct_i",), lambda: distinct_prefix(1))
+    n_ij = _cache(T, ("distinct_ij",), lambda: distinct_prefix(2))
+    body = 2 * n_i + 2 * n_ij + 2 * nnz
+    ctx.counter.add(2 * nnz * R, nnz * R, nblk * (1 + body) if nblk else body + n_i)
+    return _compressed_dense_result(ctx.expr.output_name, (T.shape[mk.T.indices.index(mk.i)], R), seg.rows, M)
 
 
 def _exec_sparse_spmm(ctx: _Ctx, m: _SpmmTerm) -> Tensor:

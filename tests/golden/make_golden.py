@@ -226,6 +226,34 @@ def mttkrp_coo3():
     return run_case("mttkrp_coo3", "M(i,r) = T(i,j,k) * B(j,r) * C(k,r)", {"T": T, "B": B, "C": C})
 
 
+def _mttkrp_tensor(rng, shape, n):
+    size = int(np.prod(shape))
+    flat = np.sort(rng.choice(size, size=n, replace=False))
+    coords = np.stack(np.unravel_index(flat, shape), axis=1)
+    vals = f32(rng.uniform(0, 1, len(coords)))
+    return st.build_from_entries(shape, st.coo(*shape), [(tuple(map(int, c)), float(v)) for c, v in zip(coords, vals)],
+                                 "T")
+
+
+@case
+def mttkrp_mode2():
+    # CP-ALS runs MTTKRP in every mode; the reference walks T in storage order for each
+    rng = np.random.default_rng(140)
+    T = _mttkrp_tensor(rng, (12, 10, 9), 110)
+    A = st.from_dense(f32(rng.uniform(0, 1, (12, 5))), name="A")
+    C = st.from_dense(f32(rng.uniform(0, 1, (9, 5))), name="C")
+    return run_case("mttkrp_mode2", "M(j,r) = T(i,j,k) * A(i,r) * C(k,r)", {"T": T, "A": A, "C": C})
+
+
+@case
+def mttkrp_mode3():
+    rng = np.random.default_rng(141)
+    T = _mttkrp_tensor(rng, (8, 11, 13), 120)
+    A = st.from_dense(f32(rng.uniform(0, 1, (8, 7))), name="A")
+    B = st.from_dense(f32(rng.uniform(0, 1, (11, 7))), name="B")
+    return run_case("mttkrp_mode3", "M(k,r) = T(i,j,k) * A(i,r) * B(j,r)", {"T": T, "A": A, "B": B})
+
+
 @case
 def kat_sddmm_worked():
     # reference tests/test_engine.py:12-19: D[0,1] == 44.0 with 3 mults

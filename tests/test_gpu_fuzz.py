@@ -64,8 +64,12 @@ def _hot_path_case(rng, cap=40):
         vals = rng.uniform(0, 1, len(coords)).astype(np.float32)
         T = st.coo_from_sorted_arrays(tuple(coords.T), vals, (m, p, q), name="T")
         r = names[3]
-        return (f"M({i},{r}) = T({i},{j},{k}) * B({j},{r}) * C({k},{r})",
-                {"T": T, "B": _dense(rng, (p, R), "B"), "C": _dense(rng, (q, R), "C")})
+        # any output mode (CP-ALS runs all three)
+        idx, ext = [i, j, k], [m, p, q]
+        o = int(rng.integers(0, 3))
+        (u, eu), (w, ew) = [(idx[t], ext[t]) for t in range(3) if t != o]
+        return (f"M({idx[o]},{r}) = T({i},{j},{k}) * B({u},{r}) * C({w},{r})",
+                {"T": T, "B": _dense(rng, (eu, R), "B"), "C": _dense(rng, (ew, R), "C")})
     if kind == "spgemm":
         A = random_tensor(rng, (m, n), "csr", dens, "A", device="cuda")
         B = random_tensor(rng, (n, K), "csr", dens, "B", device="cuda")
