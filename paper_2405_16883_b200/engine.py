@@ -950,10 +950,17 @@ def run_with_report(e: TensorExpr, bindings: dict | None = None, out_format: Ten
                   "counters": None, "wall_time_ns": wall, "variants": ["dense:torch"]}
         return result, None, report
 
-    out_fmt = out_format if out_format is not None else infer_format(e)
-    sched = schedule(e, out_fmt, weights)
-    if tiling:
-        sched = tile(e, sched, tile_size)
+    # the plan depends only on the expression (whose operands are immutable and may only be
+    # rebound to tensors of the same shape and format) and the options: memoised on it
+    plans = e.__dict__.setdefault("_plans", {})
+    key = (out_format, tile_size, tiling, weights)
+    if key not in plans:
+        out_fmt = out_format if out_format is not None else infer_format(e)
+        sched = schedule(e, out_fmt, weights)
+        if tiling:
+            sched = tile(e, sched, tile_size)
+        plans[key] = (out_fmt, sched)
+    out_fmt, sched = plans[key]
     t0 = time.perf_counter_ns()
     result, counter = execute(sched, bindings, variant=variant)
     torch.cuda.synchronize()
