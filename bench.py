@@ -301,7 +301,7 @@ class GCN(Workload):
                 # interleaved long rows), built once per step for the step's uploaded matrix
                 stats = ops.row_stats(rp)
                 variant = ops.choose_variant(stats, self.k)
-                part = ops.merge_partition(rp, v.numel(), k=self.k, colidx=ci, vals=v) \
+                part = ops.merge_partition(rp, v.numel(), k=self.k, colidx=ci, vals=v, max_row=stats.max_row) \
                     if variant == "merge" else None
                 ops.spmm_csr(rp, ci, v, x @ w1, out=b["H"], relu=True, variant=variant, partition=part,
                              stats=stats)

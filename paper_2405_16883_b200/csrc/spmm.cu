@@ -225,8 +225,8 @@ extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, 
 }
 
 // ---- long-row interleaving (plan time) -------------------------------------------------
-namespace {
-__global__ void interleave_kernel(int m, long long nnz, const int* __restrict__ rowptr, const int* __restrict__ colidx,
+namespace stc {
+__global__ void merge_interleave_kernel(int m, long long nnz, const int* __restrict__ rowptr, const int* __restrict__ colidx,
                                   const float* __restrict__ vals, int span, int* __restrict__ colidx_out,
                                   float* __restrict__ vals_out) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nnz;
@@ -251,7 +251,7 @@ __global__ void interleave_kernel(int m, long long nnz, const int* __restrict__ 
     vals_out[dst] = vals[p];
   }
 }
-}  // namespace
+}  // namespace stc
 
 extern "C" int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* colidx, const float* vals,
                                     int span, int* colidx_out, float* vals_out, void* stream) {
@@ -259,9 +259,9 @@ extern "C" int stc_merge_interleave(int m, long long nnz, const int* rowptr, con
   if (m == 0 || nnz == 0) return STC_OK;
   if (!rowptr || !colidx || !vals || !colidx_out || !vals_out) return fail(STC_EINVAL, "null pointer");
   const long long blocks = std::min<long long>(ceil_div(nnz, 256), 148LL * 16);
-  interleave_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(m, nnz, rowptr, colidx, vals,
+  merge_interleave_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(m, nnz, rowptr, colidx, vals,
                                                                                     span, colidx_out, vals_out);
-  return check_launch("interleave_kernel");
+  return check_launch("merge_interleave_kernel");
 }
 
 extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_group) {

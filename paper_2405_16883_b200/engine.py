@@ -183,7 +183,7 @@ def _stats(t: Tensor, view: RowView, key) -> ops.RowStats:
 def _partition(t: Tensor, view: RowView, key, k: int) -> ops.MergePartition:
     return _cache(t, ("partition", k) + key,
                   lambda: ops.merge_partition(view.rowptr, view.vals.numel(), k=k, colidx=view.cols,
-                                              vals=view.vals))
+                                              vals=view.vals, max_row=_stats(t, view, key).max_row))
 
 
 # ---------------------------------------------------------------------------

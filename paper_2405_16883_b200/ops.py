@@ -136,7 +136,7 @@ def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "
 
 def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None = None, *,
                     k: int = 128, batch: int = 1, kind: str = "spmm", colidx: torch.Tensor | None = None,
-                    vals: torch.Tensor | None = None) -> MergePartition:
+                    vals: torch.Tensor | None = None, max_row: int | None = None) -> MergePartition:
     """Plan-time merge-path partition; ``items_per_group`` None/0 = planned for ``k``.
     With the matrix's ``colidx``/``vals`` (SpMM) the plan also carries their long-row
     interleaved copies, and ``spmm_csr`` reads those; use such a plan only with that matrix."""
@@ -151,8 +151,11 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
                                         stream_handle())
     check(rc, "stc_merge_path_partition")
     ci = va = None
-    if kind == "spmm" and colidx is not None and vals is not None and vals.dim() == 1 and INTERLEAVE:
-        ci, va = interleave_long_rows(rowptr, _i32(colidx), _f32(vals), items_per_group)
+    if kind == "spmm" and colidx is not None and vals is not None and vals.dim() == 1 and INTERLEAVE and m > 0:
+        if max_row is None:
+            max_row = int((rowptr[1:] - rowptr[:-1]).max().item())
+        if max_row > items_per_group:  # some row spans several groups: interleave (a copy of A)
+            ci, va = interleave_long_rows(rowptr, _i32(colidx), _f32(vals), items_per_group)
     return MergePartition(starts, items_per_group, groups, ci, va)
 
 
@@ -226,7 +229,8 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
     ipg = 0
     plan_ptr = None
     if variant == "merge":
-        partition = partition or merge_partition(rowptr, nnz, k=k, colidx=colidx, vals=vals)
+        partition = partition or merge_partition(rowptr, nnz, k=k, colidx=colidx, vals=vals,
+                                                 max_row=None if stats is None else stats.max_row)
         ipg = partition.items_per_group
         plan_ptr = ptr(partition.starts)
         if partition.colidx is not None:   # the plan's long-row interleaved entries
