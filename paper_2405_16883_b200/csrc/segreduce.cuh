@@ -57,6 +57,7 @@ struct SpmmOp {
   unsigned lane_off = 0;  // this lane's first column (added in 32-bit)
 
   static constexpr int kRing = 8;           // gathers in flight per group
+  static constexpr bool kHoistItem = true;  // next fetch's item read one step ahead
   static constexpr int kMinBlocks = 4;      // resident CTAs per SM (register budget)
   static constexpr int kStageUnroll = 8;    // item loads per lane in flight while staging
   // staged items per CTA; the rest of SMEM stays L1, which the in-flight gathers need
@@ -105,6 +106,7 @@ struct MttkrpOp {
   // one (i, j) fiber share B[j,:]. M[i,:] += B[j,:] * sum_k T[i,j,k] C[k,:] gathers
   // B[j,:] once per fiber (flag = first entry of a fiber) instead of once per entry.
   static constexpr int kRing = VEC == 4 ? 4 : 8;
+  static constexpr bool kHoistItem = false;
   static constexpr int kMinBlocks = 3;
   static constexpr int kStageUnroll = 1;     // (2 and 3 measured: no gain, more registers)
   static constexpr int kStageBytes = 32768;  // 3 CTAs x 50 KB SMEM leaves ~75 KB of L1 for the hot factor rows
@@ -459,6 +461,10 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     for (int u = 0; u < U; ++u)
       if (col_ok) op.fetch(items[u], ring[u]);
     int q0 = 0;
+    // the item of the next fetch is read from shared memory one step ahead, so the
+    // gather's address does not wait on that LDS (the window's pad covers the overrun)
+    // (SpMM only: MTTKRP's 16-byte items would spill at its register budget)
+    Item nf = items[U];
     for (; q0 + U <= wn; q0 += U) {  // full ring turns: no bounds predicates
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -466,8 +472,15 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
           flush();
           end_w = cur_end - w0;
         }
-        op.accumulate(acc, fst, ring[u], items[q0 + u]);
-        if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
+        if constexpr (Op::kHoistItem) {
+          const Item cur = nf;
+          nf = items[q0 + u + 1 + U];
+          op.accumulate(acc, fst, ring[u], items[q0 + u]);
+          if (col_ok) op.fetch(cur, ring[u]);
+        } else {
+          op.accumulate(acc, fst, ring[u], items[q0 + u]);
+          if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
+        }
       }
     }
 #pragma unroll
