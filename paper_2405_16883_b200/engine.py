@@ -192,10 +192,11 @@ def _partition(t: Tensor, view: RowView, key, k: int) -> ops.MergePartition:
 
 
 def _require_device(tensors) -> None:
-    from ._abi import require_cuda
+    from ._abi import lib, require_cuda
 
     for t in tensors:
         require_cuda(t.storage.values)
+    lib()  # the compiled extension must be present for every contraction (no torch-only path)
 
 
 def _dense_torch(t: Tensor, order) -> torch.Tensor:
