@@ -1,0 +1,39 @@
+"""Per-group finish times of the cfg5 MTTKRP merge kernel (diagnostic STC_DBG_TIMING build,
+see tools/merge_balance_probe.py for the build line)."""
+import ctypes
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2405_16883_b200 import ops, synthetic  # noqa: E402
+
+(i, j, k), vals, B, C = synthetic.cfg5()
+It, Jt, Kt = (torch.from_numpy(x).int().cuda() for x in (i, j, k))
+Vt = torch.from_numpy(vals).cuda()
+seg = ops.coo_segments(It)
+Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
+part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp")
+FL = torch.empty(128 * 1024 * 1024, device="cuda")
+for _ in range(3):
+    ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part)
+FL.zero_()
+torch.cuda.synchronize()
+ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part)
+torch.cuda.synchronize()
+G = part.n_groups
+buf = np.zeros((1 << 16, 4), dtype=np.uint64)
+assert ops.lib().stc_debug_timing(ctypes.c_void_p(buf.ctypes.data), ctypes.c_size_t(buf.nbytes)) == 0
+d = buf[:min(G, 1 << 16)]
+t0, t1 = d[:, 0].astype(np.int64), d[:, 1].astype(np.int64)
+end = (t1 - t0.min()) / 1e3
+rows = d[:, 2].astype(np.int64)
+nnz = (d[:, 3] >> np.uint64(32)).astype(np.int64)
+print(f"groups {G} ipg {part.items_per_group}; span {end.max():.1f} us")
+print("finish p1/p10/p50/p90/p99/max: %.1f %.1f %.1f %.1f %.1f %.1f" % tuple(np.percentile(end, [1, 10, 50, 90, 99, 100])))
+print("corr(end, rows) %.2f  corr(end, nnz) %.2f" % (np.corrcoef(end, rows)[0, 1], np.corrcoef(end, nnz)[0, 1]))
+z = rows == 0
+print("0-row groups: %d, finish p10/p90 %.1f/%.1f; >0-row groups p10/p90 %.1f/%.1f" % (
+    z.sum(), *np.percentile(end[z], [10, 90]), *np.percentile(end[~z], [10, 90])))
