@@ -181,7 +181,8 @@ def cfg5():
     seg = ops.coo_segments(It)
     Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
     part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp")
-    ms = gpu_time(lambda: ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part))
+    ws = ops.spmm_workspace(seg.n_seg, len(vals), 32, "merge", part.items_per_group, 1, "cuda")
+    ms = gpu_time(lambda: ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part, workspace=ws))
     nnz = len(vals)
     flops = 3.0 * nnz * 32
     nbytes = 16 * nnz + 2 * 4 * 20000 * 32 + 4 * seg.n_seg * 32

@@ -37,3 +37,13 @@ print("corr(end, rows) %.2f  corr(end, nnz) %.2f" % (np.corrcoef(end, rows)[0, 1
 z = rows == 0
 print("0-row groups: %d, finish p10/p90 %.1f/%.1f; >0-row groups p10/p90 %.1f/%.1f" % (
     z.sum(), *np.percentile(end[z], [10, 90]), *np.percentile(end[~z], [10, 90])))
+# fiber starts per group: entries whose (i, j) differs from the previous entry's gather B[j]
+st = part.starts.cpu().numpy().reshape(-1, 2).astype(np.int64)
+fs = np.ones(len(j), bool)
+fs[1:] = (i[1:] != i[:-1]) | (j[1:] != j[:-1])
+cfs = np.concatenate([[0], np.cumsum(fs)])
+fib = cfs[st[1:G + 1, 1]] - cfs[st[:G, 1]]
+print("corr(end, fibers) %.2f  (fibers per group p10/p50/p90 %d/%d/%d)" % (
+    np.corrcoef(end, fib[:len(end)])[0, 1], *np.percentile(fib, [10, 50, 90])))
+gathers = nnz + fib[:len(end)]
+print("corr(end, entries + fibers) %.2f" % np.corrcoef(end, gathers)[0, 1])
