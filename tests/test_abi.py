@@ -55,6 +55,11 @@ def test_argument_validation_without_gpu():
     rc = lib.stc_spmm_csr_f32(4, 4, 4, 8, 8, 8, 4, 16, 4, 16, 4, None, 0, _abi.VARIANT_MERGE, 0, None,
                               128, None, 0, None)
     assert rc == _abi.STC_EINVAL and b"partition" in lib.stc_last_error()
+    rc = lib.stc_merge_interleave(4, 10, 8, 8, 8, 0, 16, 16, None)       # span < 1
+    assert rc == _abi.STC_EINVAL and b"interleave" in lib.stc_last_error()
+    rc = lib.stc_merge_interleave(4, 10, None, 8, 8, 64, 16, 16, None)   # null rowptr
+    assert rc == _abi.STC_EINVAL and b"null" in lib.stc_last_error()
+    assert lib.stc_merge_interleave(0, 0, None, None, None, 64, None, None, None) == _abi.STC_OK  # empty
     rc = lib.stc_sddmm_csr_f32(4, 4, 48, 1, 8, 8, None, 4, 16, 0, 48, 16, 0, 48, 1.0, 32, None)
     assert rc == _abi.STC_EUNSUPPORTED
     with pytest.raises(ValueError):
