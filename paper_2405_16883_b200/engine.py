@@ -609,13 +609,26 @@ def _exec_sddmm(ctx: _Ctx, s: _SddmmTerm) -> Tensor:
     Qd = _dense_torch(ctx.t(s.Q), tuple(s.Q.indices.index(v) for v in hs + (s.i, s.d)))
     Kd = _dense_torch(ctx.t(s.K), tuple(s.K.indices.index(v) for v in hs + (s.j, s.d)))
     d = Qd.shape[-1]
-    dk = next((w for w in (4, 8, 16, 32, 64, 128) if w >= d), None)
-    if dk is None:
-        raise UnsupportedExpressionError(f"SDDMM reduction extent {d} > 128")
-    if dk != d:  # zero-pad the reduction dim to the kernel's lane width (exact: adds 0 products)
-        Qd = torch.nn.functional.pad(Qd, (0, dk - d))
-        Kd = torch.nn.functional.pad(Kd, (0, dk - d))
-    vals = ops.sddmm_csr(view.rowptr, view.cols, Qd, Kd, maskvals=view.vals, scale=1.0)
+    if d <= 128:
+        dk = next(w for w in (4, 8, 16, 32, 64, 128) if w >= d)
+        if dk != d:  # zero-pad the reduction dim to the kernel's lane width (exact: adds 0 products)
+            Qd = torch.nn.functional.pad(Qd, (0, dk - d))
+            Kd = torch.nn.functional.pad(Kd, (0, dk - d))
+        vals = ops.sddmm_csr(view.rowptr, view.cols, Qd, Kd, maskvals=view.vals, scale=1.0)
+    else:
+        # wider reductions: 128-wide blocks of the kernel summed left to right (the reference's
+        # tiled d-blocks), then the mask value, as in the reference (dot first, times m_ij)
+        vals = None
+        for c0 in range(0, d, 128):
+            w = min(128, d - c0)
+            dk = next(x for x in (4, 8, 16, 32, 64, 128) if x >= w)
+            Qc, Kc = Qd[..., c0:c0 + w], Kd[..., c0:c0 + w]
+            if dk != w:
+                Qc = torch.nn.functional.pad(Qc, (0, dk - w))
+                Kc = torch.nn.functional.pad(Kc, (0, dk - w))
+            part = ops.sddmm_csr(view.rowptr, view.cols, Qc.contiguous(), Kc.contiguous(), scale=1.0)
+            vals = part if vals is None else vals + part
+        vals = vals * view.vals
     ctx.chosen.append(f"sddmm:{view.kind}")
     nnz = view.vals.numel()
     H = 1 if s.h is None else Qd.shape[0]

@@ -192,6 +192,16 @@ def sddmm_d100():
 
 
 @case
+def sddmm_d300():
+    # reduction wider than one 128-lane kernel block: three blocks summed, then the mask value
+    rng = np.random.default_rng(115)
+    M = st.build_from_entries((9, 12), st.csr(9, 12), rand_sparse_entries(rng, (9, 12), 0.3), "M")
+    Q = st.from_dense(f32(rng.standard_normal((9, 300))), name="Q")
+    K = st.from_dense(f32(rng.standard_normal((12, 300))), name="K")
+    return run_case("sddmm_d300", "S(i,j) = M(i,j) * Q(i,d) * K(j,d)", {"M": M, "Q": Q, "K": K})
+
+
+@case
 def sddmm_multihead():
     rng = np.random.default_rng(112)
     M = st.build_from_entries((10, 10), st.csr(10, 10), rand_sparse_entries(rng, (10, 10), 0.3), "M")

@@ -50,7 +50,7 @@ def _hot_path_case(rng, cap=40):
             return src + f" + D({i},{k})", {"A": A, "B": B, "D": _dense(rng, (m, K), "D")}
         return src, {"A": A, "B": B}
     if kind == "sddmm":
-        d = int(rng.integers(1, 70))
+        d = int(rng.integers(1, 300))
         M = random_tensor(rng, (m, n), "csr", dens, "M", device="cuda")
         fac = [f"M({i},{j})", f"Q({i},{k})", f"K({j},{k})"]
         rng.shuffle(fac)
