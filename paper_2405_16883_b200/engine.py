@@ -626,7 +626,10 @@ def _exec_sddmm(ctx: _Ctx, s: _SddmmTerm) -> Tensor:
             if dk != w:
                 Qc = torch.nn.functional.pad(Qc, (0, dk - w))
                 Kc = torch.nn.functional.pad(Kc, (0, dk - w))
-            part = ops.sddmm_csr(view.rowptr, view.cols, Qc.contiguous(), Kc.contiguous(), scale=1.0)
+            # (a fresh copy: canonical strides even for size-1 dims of the sliced operands)
+            Qc = Qc.clone(memory_format=torch.contiguous_format)
+            Kc = Kc.clone(memory_format=torch.contiguous_format)
+            part = ops.sddmm_csr(view.rowptr, view.cols, Qc, Kc, scale=1.0)
             vals = part if vals is None else vals + part
         vals = vals * view.vals
     ctx.chosen.append(f"sddmm:{view.kind}")
