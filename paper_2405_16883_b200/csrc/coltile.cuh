@@ -13,9 +13,10 @@
 // a wide operand buffer for CUDA-core FMAs.
 //
 // Entry path: the plan (`stc_coltile_plan`) re-encodes A per (128-row block,
-// 64-column chunk, row) as packed entries {4 * (col - chunk start), value bits},
-// each row padded with zero-weight entries to a multiple of 4. A warp's list for
-// a chunk is contiguous: it is copied into SMEM with cp.async one chunk ahead, and
+// 64-column chunk, row) as packed entries {TMEM address of B[col] for the row's warp and
+// the chunk's buffer, value bits}, each row padded with zero-weight entries to a multiple
+// of 4 — the inner loop adds nothing to the addresses it loads. A warp's list for a chunk
+// is contiguous: it is copied into SMEM with cp.async one chunk ahead, and
 // the inner loop is two LDS.128 (4 entries) + 4 tcgen05.ld + one wait::ld + 16 FFMA.
 // The plan carries the VALUES of A (it is the prepared form of the matrix, like a
 // cuSPARSE SpMM preprocess): rebuild it when the values change.
@@ -109,8 +110,11 @@ __global__ void ctt_scatter_kernel(int m, int n_chunks, const int* __restrict__ 
     const int a = cp[0], b = cp[1];
     const long long slot = ((long long)(row / CTT_ROWS) * n_chunks + c) * CTT_ROWS + row % CTT_ROWS;
     int e = offs[slot];
-    for (int p = a; p < b; ++p) ent[e++] = make_int2(4 * (colidx[p] - c * CTT_CHUNK), __float_as_int(vals[p]));
-    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(0, 0);
+    // the entry carries its full TMEM address (the kernel's allocation starts at column 0):
+    // lane quarter of the row's consumer warp, TMEM buffer of the chunk, 4 columns per B row
+    const int base = ((32 * (((row % CTT_ROWS) / CTT_RPW) % 4)) << 16) + (c & 1) * 4 * CTT_CHUNK;
+    for (int p = a; p < b; ++p) ent[e++] = make_int2(base + 4 * (colidx[p] - c * CTT_CHUNK), __float_as_int(vals[p]));
+    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(base, 0);
   }
 }
 
@@ -145,6 +149,9 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = *tbase_s;
+  // all 512 columns are allocated, so the allocation starts at lane 0, column 0: the plan's
+  // entries carry absolute TMEM addresses (no per-load address add in the inner loop)
+  if (tbase != 0u) __trap();
 
   if (warp == CTT_WARPS) {
     // ---------------- producer: B chunks -> SMEM stages (bulk copies, one per B row) ----------------
@@ -225,14 +232,14 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
 #pragma unroll
     for (int r = 0; r < CTT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
     // 4 entries -> 4 tcgen05.ld, one wait, 16 FFMA
-    auto group = [&](float (&a)[4], uint32_t tchunk, int4 e01, int4 e23) {
+    auto group = [&](float (&a)[4], int4 e01, int4 e23) {
       uint32_t x[4][4];
-      const int cols[4] = {e01.x, e01.z, e23.x, e23.z};
+      const int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
-                     : "r"(tchunk + (uint32_t)cols[u]));
+                     : "r"(taddr[u]));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       const float w[4] = {__int_as_float(e01.y), __int_as_float(e01.w), __int_as_float(e23.y),
                           __int_as_float(e23.w)};
@@ -256,7 +263,6 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
       cp_async_wait<1>();  // chunk ch's list has landed (ch + 1's may be in flight)
       __syncwarp();
       if (ch + 1 < n_chunks) fill(ch + 1);
-      const uint32_t tchunk = tq + (uint32_t)((ch & 1) * 4 * CTT_CHUNK);
       const int e0 = __shfl_sync(0xffffffffu, meta, 0);
       const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
       if (total <= CTT_ECAP) {
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         for (int r = 0; r < CTT_RPW; ++r) {
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
-          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], tchunk, sc[q / 2], sc[q / 2 + 1]);
+          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], sc[q / 2], sc[q / 2 + 1]);
         }
       } else {  // rows denser than the staged list: entries straight from global memory
         const int4* g = reinterpret_cast<const int4*>(ent + e0);
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         for (int r = 0; r < CTT_RPW; ++r) {
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
-          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], tchunk, g[q / 2], g[q / 2 + 1]);
+          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], g[q / 2], g[q / 2 + 1]);
         }
       }
       quarter_sync();  // chunk ch fully read, chunk ch + 1 fully written
