@@ -221,6 +221,26 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[c % CTT_STAGES])) : "memory");
     };
+    // the same copy split in CTT_RPW / 2 phases of 4 rows, interleaved with the group work of
+    // the current chunk: a phase's LDS.128 are issued before two rows' groups and its tcgen05.st
+    // after them, so the shared-memory latency of the copy hides behind the FMAs
+    constexpr int kFillRows = CTT_CHUNK / 4, kPhases = CTT_RPW / 2, kPhaseRows = kFillRows / kPhases;
+    float4 fv[kPhaseRows];
+    auto fill_load = [&](int c, int ph) {
+      const float* src = smem + (c % CTT_STAGES) * CTT_STAGE_FLOATS + (kFillRows * part + kPhaseRows * ph) * CTT_COLS +
+                         lane * 4;
+#pragma unroll
+      for (int j = 0; j < kPhaseRows; ++j) fv[j] = *reinterpret_cast<const float4*>(src + j * CTT_COLS);
+    };
+    auto fill_store = [&](int c, int ph) {
+      const uint32_t dst = tq + (uint32_t)((c & 1) * 4 * CTT_CHUNK + 4 * (kFillRows * part + kPhaseRows * ph));
+#pragma unroll
+      for (int j = 0; j < kPhaseRows; ++j)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + 4 * j),
+                     "r"(__float_as_uint(fv[j].x)), "r"(__float_as_uint(fv[j].y)), "r"(__float_as_uint(fv[j].z)),
+                     "r"(__float_as_uint(fv[j].w))
+                     : "memory");
+    };
     auto quarter_sync = [&]() {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -262,7 +282,14 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
       stage_list(ch + 1, meta_next);
       cp_async_wait<1>();  // chunk ch's list has landed (ch + 1's may be in flight)
       __syncwarp();
-      if (ch + 1 < n_chunks) fill(ch + 1);
+      const bool next = ch + 1 < n_chunks;
+      if (next) ctt_mbar_wait(ctt_smem_u32(&sfull[(ch + 1) % CTT_STAGES]), (uint32_t)(((ch + 1) / CTT_STAGES) & 1));
+      auto fill_step = [&](int r) {  // before rows r = 0, 2, 4, 6 of chunk ch: one phase of chunk ch + 1
+        if (next && r % 2 == 0) {
+          if (r > 0) fill_store(ch + 1, r / 2 - 1);
+          fill_load(ch + 1, r / 2);
+        }
+      };
       const int e0 = __shfl_sync(0xffffffffu, meta, 0);
       const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
       if (total <= CTT_ECAP) {
@@ -271,6 +298,7 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         for (int r = 0; r < CTT_RPW; ++r) {
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
+          fill_step(r);
           for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], sc[q / 2], sc[q / 2 + 1]);
         }
       } else {  // rows denser than the staged list: entries straight from global memory
@@ -279,8 +307,16 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         for (int r = 0; r < CTT_RPW; ++r) {
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
+          fill_step(r);
           for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], g[q / 2], g[q / 2 + 1]);
         }
+      }
+      if (next) {
+        fill_store(ch + 1, kPhases - 1);
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[(ch + 1) % CTT_STAGES]))
+                       : "memory");
       }
       quarter_sync();  // chunk ch fully read, chunk ch + 1 fully written
       meta = meta_next;
