@@ -40,8 +40,8 @@ extern "C" {
  *   ROW     one sub-warp per row (loop order [i,j,k], rows uniform)
  *   MERGE   nnz-balanced merge-path split with atomics-free carries
  *           (same loop order, power-law rows)
- *   COLTILE column-tiled, dense operand staged in shared memory
- *           (tile set {k} with a wide k)                                    */
+ *   COLTILE column-tiled, dense operand staged in shared memory and
+ *           Tensor Memory (tile set {k} with a wide k)                                    */
 #define STC_VARIANT_ROW 0
 #define STC_VARIANT_MERGE 1
 #define STC_VARIANT_COLTILE 2
@@ -96,8 +96,9 @@ int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* col
 int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind);
 
 /* Plan of the COLTILE variant (B operand staged in Tensor Memory): A re-encoded
- * per (128-row block, 64-column chunk, row) as packed {operand offset, value}
- * entries, each row padded with zero-weight entries to a multiple of 4.
+ * per (128-row block, 64-column chunk, row) as packed {Tensor Memory address
+ * of the operand row, value} entries, each row padded with zero-weight
+ * entries to a multiple of 4 (the layout is private to the kernel).
  * The plan CARRIES A's VALUES (the prepared form of A, like a cuSPARSE SpMM
  * preprocess): rebuild it whenever the values change. stc_coltile_plan_ints
  * gives its size in int32 (-1 if unsupported); pass it as the `partition` of a
