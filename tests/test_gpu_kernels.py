@@ -41,6 +41,9 @@ STRUCTS = {
     "all_empty": lambda r: (17, 9, np.zeros(17, dtype=np.int64)),
     "single_row": lambda r: (1, 100, [37]),
     "trailing_empty": lambda r: (40, 30, np.where(np.arange(40) > 20, 0, 7)),
+    # full rows: a COLTILE warp's chunk list (8 rows x 64 entries) overflows its shared-memory
+    # stage, so the entries stream from global memory (coltile.cuh, `total > CTT_ECAP`)
+    "dense_rows": lambda r: (200, 300, np.full(200, 300)),
 }
 
 
