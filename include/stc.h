@@ -59,15 +59,6 @@ const char* stc_last_error(void);
  * Used by bench.py to report how many native launches a timed region made. */
 long long stc_launch_count(void);
 
-/* L2 residency control for the gathered dense operand (device-wide setting).
- * Sets the persisting-L2 carve-out to `bytes` (0 disables); subsequent SpMM /
- * MTTKRP launches then carry an access-policy window over their gathered dense
- * operand (hit ratio = carve-out / operand bytes), so hub and cold rows stay
- * resident while the streamed index arrays and outputs are evicted first.
- * Returns the carve-out actually granted (bytes) or a negative error.        */
-long long stc_l2_set_persisting(size_t bytes);
-/* Demote every persisting L2 line to normal (e.g. before an L2 flush). */
-int stc_l2_reset_persisting(void);
 
 /* Merge-path partition of a compressed row structure (plan time).
  * Groups own `items_per_group` consecutive items of the merged sequence

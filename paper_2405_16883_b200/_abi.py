@@ -49,8 +49,6 @@ SIGNATURES = {
     "stc_abi_version": (_i, []),
     "stc_last_error": (ctypes.c_char_p, []),
     "stc_launch_count": (_ll, []),
-    "stc_l2_set_persisting": (_ll, [_sz]),
-    "stc_l2_reset_persisting": (_i, []),
     "stc_merge_path_groups": (_ll, [_i, _ll, _i]),
     "stc_merge_path_partition": (_i, [_i, _ll, _p, _i, _p, _p]),
     "stc_coltile_plan_ints": (_ll, [_i, _i, _ll]),

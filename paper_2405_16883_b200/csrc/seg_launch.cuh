@@ -34,8 +34,6 @@ struct Launch {
   int variant;
   int batch;
   cudaStream_t stream;
-  const void* window;      // gathered dense operand (L2 access-policy window)
-  size_t window_bytes;
 };
 
 template <int SUBW, int VEC, int EPI, bool ADD, class Op>
@@ -48,8 +46,7 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
     // a row's sub-warp loads SUBW entries at a time: keep up to 16 of their gathers in flight
     constexpr int UR = SUBW >= 16 ? 16 : (SUBW >= 8 ? 8 : 4);
     const dim3 grid((unsigned)ceil_div((long long)o.m * SUBW, kThreads), slabs, L.batch);
-    launch_windowed(row_kernel<SUBW, VEC, EPI, ADD, UR, Op>, grid, dim3(kThreads), 0, L.stream, L.window,
-                    L.window_bytes, o, ms, op);
+    row_kernel<SUBW, VEC, EPI, ADD, UR, Op><<<grid, dim3(kThreads), 0, L.stream>>>(o, ms, op);
     return check_launch("row_kernel");
   }
   constexpr int NG = kThreads / SUBW;
@@ -66,11 +63,9 @@ int launch_seg(const SegOut& o, MergeShape ms, const Op& op, const Launch& L) {
     configured = true;
   }
   if (o.k % SW == 0)
-    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op>, grid, dim3(kThreads), smem, L.stream,
-                    L.window, L.window_bytes, o, ms, op);
+    merge_kernel<SUBW, VEC, EPI, ADD, U, true, Op><<<grid, dim3(kThreads), smem, L.stream>>>(o, ms, op);
   else
-    launch_windowed(merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op>, grid, dim3(kThreads), smem, L.stream,
-                    L.window, L.window_bytes, o, ms, op);
+    merge_kernel<SUBW, VEC, EPI, ADD, U, false, Op><<<grid, dim3(kThreads), smem, L.stream>>>(o, ms, op);
   return check_launch("merge_kernel");
 }
 

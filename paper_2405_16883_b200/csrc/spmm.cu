@@ -51,8 +51,8 @@ int launch_coltile_tmem(int m, int n, int k, long long nnz, const int* plan, con
   if (m == 0 || k == 0) return STC_OK;
   const CttLayout lay = ctt_layout(m, n, nnz);
   const dim3 grid((unsigned)ceil_div(m, CTT_ROWS), (unsigned)ceil_div(k, CTT_COLS));
-  launch_windowed(coltile_tmem_kernel<EPI, ADD>, grid, dim3(CTT_THREADS), CTT_SMEM, st, L.window, L.window_bytes, m,
-                  n, k, plan + lay.offs, reinterpret_cast<const int2*>(plan + lay.ent), B, ldb, C, ldc, D, ldd);
+  coltile_tmem_kernel<EPI, ADD><<<grid, dim3(CTT_THREADS), CTT_SMEM, st>>>(
+      m, n, k, plan + lay.offs, reinterpret_cast<const int2*>(plan + lay.ent), B, ldb, C, ldc, D, ldd);
   return check_launch("coltile_tmem_kernel");
 }
 
@@ -80,7 +80,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
     if (!vec4) return fail(STC_EUNSUPPORTED, "COLTILE needs k, ldb, ldc multiples of 4 and 16-byte alignment");
     if (batch != 1) return fail(STC_EUNSUPPORTED, "COLTILE is not batched");
     if (!partition) return fail(STC_EINVAL, "COLTILE needs its plan (stc_coltile_plan) as `partition`");
-    const Launch L{variant, 1, st, B, (size_t)((long long)n * ldb) * sizeof(float)};
+    const Launch L{variant, 1, st};
     if (epilogue == STC_EPILOGUE_RELU)
       return D ? launch_coltile_tmem<EPI_RELU, true>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L)
                : launch_coltile_tmem<EPI_RELU, false>(m, n, k, nnz, partition, B, ldb, C, ldc, D, ldd, st, L);
@@ -112,7 +112,7 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
     ms.tail_buf = ms.head_buf + (long long)batch * slabs * n_cta * sw;
     ms.counters = reinterpret_cast<int*>(ms.tail_buf + (long long)batch * slabs * n_cta * sw);
   }
-  Launch L{variant, batch, st, B, (size_t)((long long)n * ldb * (batch > 1 && b_bs ? batch : 1)) * sizeof(float)};
+  const Launch L{variant, batch, st};
   if (wide) return spmm_wide(vec4 ? 4 : 1, epilogue, D != nullptr, o, ms, colidx, vals, B, ldb, L);
   if (vec4) {
     SpmmOp<4> op{colidx, vals, B, ldb};
@@ -403,7 +403,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
     ms.tail_buf = ms.head_buf + ceil_div(rank, sw) * n_cta * sw;
     ms.counters = reinterpret_cast<int*>(ms.tail_buf + ceil_div(rank, sw) * n_cta * sw);
   }
-  Launch L{variant, 1, st, B, (size_t)((long long)n_j * ldb) * sizeof(float)};
+  const Launch L{variant, 1, st};
   if (wide) return mttkrp_wide(vec, o, ms, jcrd, kcrd, vals, B, ldb, C, ldcf, subw, L);
   if (vec4) {
     MttkrpOp<4> op{jcrd, kcrd, vals, B, ldb, C, ldcf};

@@ -78,23 +78,6 @@ def choose_variant(stats: RowStats, k: int, aligned: bool = True) -> str:
     return "row"
 
 
-def l2_set_persisting(nbytes: int) -> int:
-    """Carve out ``nbytes`` of L2 for persisting accesses (device-wide); SpMM-family
-    launches then pin their gathered dense operand there. Returns bytes granted."""
-    if not torch.cuda.is_available():
-        raise _abi.ExtensionUnavailable("no CUDA device")
-    torch.cuda.current_device()
-    got = int(lib().stc_l2_set_persisting(int(nbytes)))
-    if got < 0:
-        check(got, "stc_l2_set_persisting")
-    return got
-
-
-def l2_reset_persisting() -> None:
-    """Demote all persisting L2 lines to normal (call before flushing L2)."""
-    check(lib().stc_l2_reset_persisting(), "stc_l2_reset_persisting")
-
-
 @dataclass
 class MergePartition:
     starts: torch.Tensor      # int32 [2 * (n_groups + 1)]
