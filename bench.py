@@ -11,14 +11,17 @@ TF32 off) computed before timing. The full forward including the GEMMs is timed
 separately and reported under ``gcn_forward``.
 
 ``value`` = SpMM GFLOP/s (2·nnz·128 flops per layer) with inputs resident in
-HBM, L2 flushed (512 MB write) before every step, CUDA events on the launching
-stream, max over ranks. ``e2e`` = the same metric through the C-ABI op with
-pinned HOST buffers (H2D of Â and Z1/Z2, plan, both layers, D2H of O, per step).
+HBM, L2 flushed (512 MB write) before every layer, CUDA events on the launching
+stream, max over ranks. ``e2e`` = the same metric through the public API (``torch.mm`` on a declared
+CSR tensor) with pinned HOST buffers (H2D of Â, X, W1, W2; plan; the whole
+forward; D2H of O, per step), its output checked against the oracle afterwards.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1..5]
 
 ``--impl reference`` times the CPU oracle port (C restatement of the
-reference engine's arithmetic, all host threads) on the same workload.
+reference engine's arithmetic, all host threads) on the same workload, and next
+to it the reference's own Python engine (``sparsetc.execute`` from
+baseline/_ref, one core) on a strided row sample, extrapolated by nnz.
 """
 
 from __future__ import annotations
@@ -163,7 +166,7 @@ class Workload:
     dominant = ""              # ncu kernel-name key of the dominant kernel
     launches_per_step = 0
 
-    def step(self, events):    # records events around the dominant kernel launches
+    def step(self, events, flush):    # records events around the dominant kernel launches
         raise NotImplementedError
 
 
@@ -220,18 +223,24 @@ class GCN(Workload):
                                  variant=self.variant, partition=self.partition, workspace=self.ws,
                                  stats=self.stats)
 
-    def step(self, ev):
+    def step(self, ev, flush):
+        """Both layers, L2 flushed before each (outside the events): ev[0..1] bracket layer 1,
+        ev[2..3] layer 2."""
+        flush.zero_()
         ev[0].record()
         self.layer(self.Z1, self.H, True)
         ev[1].record()
-        self.layer(self.Z2, self.O, False)
+        flush.zero_()
         ev[2].record()
+        self.layer(self.Z2, self.O, False)
+        ev[3].record()
 
     def config(self):
         return {"workload": self.name, "graph_nodes": self.n, "nnz": self.nnz, "feature_width": self.k,
                 "max_row": self.stats.max_row, "variant": self.variant, "items_per_group": self.ipg,
                 "step": "2 SpMM layers of the GCN forward (layer-1 ReLU fused); GEMMs in gcn_forward",
-                "l2": "flushed before every step (512 MB write)", "dtype_indices": "int32"}
+                "l2": "flushed before every layer (512 MB write, outside the timed events)",
+                "dtype_indices": "int32"}
 
     def full_forward_ms(self, reps=20):
         """Whole forward incl. cuBLAS GEMMs (X·W1, H·W2), device time per forward."""
@@ -258,28 +267,32 @@ class GCN(Workload):
                 "l2": "warm (back-to-back forwards)"}
 
     def e2e(self, steps, warmup):
-        """Same metric through the public op (ops.spmm_csr -> stc_spmm_csr_f32) with pinned host
-        buffers: every step uploads its inputs (graph, features X, weights W1, W2), runs the whole
-        GCN forward — Z1 = X W1, H = ReLU(A Z1), Z2 = H W2, O = A Z2 (the op plans itself; the GEMMs
-        are cuBLAS and count no flops here) — and reads O back, all inside the timed region. Steps
-        are pipelined over three streams with double-buffered device buffers, so step i+1's upload
-        overlaps step i's compute and download (PCIe is full duplex)."""
-        torch, ops = self.torch, self.ops
+        """Same metric through the public API a user calls, with pinned HOST buffers: every
+        step uploads its inputs (graph rowptr/colidx/values, features X, weights W1, W2), wraps
+        the graph as a declared CSR tensor (``st.csr_from_arrays``) and runs the GCN forward
+        with torch calls intercepted by the package: ``H = relu(torch.mm(A, X @ W1))``,
+        ``O = torch.mm(A, H @ W2)`` (each torch.mm = parse_einsum + run: plan — row statistics,
+        merge partition, long-row interleave — then the SpMM kernel; the GEMMs are cuBLAS and
+        count no flops here), then reads O back, all inside the timed region. Steps are
+        pipelined over three streams with double-buffered device buffers (PCIe is full duplex).
+        Returns (ms per step, H2D bytes, D2H bytes, the last step's downloaded O)."""
+        torch = self.torch
+        import paper_2405_16883_b200 as st
+
         A, X, W1, W2 = self.host
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         h_in = (pin(A.rowptr.astype(np.int32)), pin(A.colidx.astype(np.int32)), pin(A.vals),
                 pin(_f32(X)), pin(_f32(W1)), pin(_f32(W2)))
         h_out = [torch.empty((self.n, self.k), dtype=torch.float32).pin_memory() for _ in range(2)]
         dev = self.X.device
-        bufs = [dict(inp=[torch.empty_like(h, device=dev) for h in h_in],
-                     H=torch.empty((self.n, self.k), device=dev), O=torch.empty((self.n, self.k), device=dev))
-                for _ in range(2)]
+        bufs = [dict(inp=[torch.empty_like(h, device=dev) for h in h_in]) for _ in range(2)]
         h2d = sum(t.numel() * t.element_size() for t in h_in)
         d2h = h_out[0].numel() * 4
         s_up, s_comp, s_down = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         ev_up = [torch.cuda.Event() for _ in range(2)]
         ev_comp = [torch.cuda.Event() for _ in range(2)]
         ev_down = [torch.cuda.Event() for _ in range(2)]
+        outs = [None, None]
 
         def upload(i):
             b = bufs[i % 2]
@@ -291,26 +304,18 @@ class GCN(Workload):
                 ev_up[i % 2].record(s_up)
 
         def compute(i):
-            b = bufs[i % 2]
-            rp, ci, v, x, w1, w2 = b["inp"]
+            rp, ci, v, x, w1, w2 = bufs[i % 2]["inp"]
             with torch.cuda.stream(s_comp):
                 s_comp.wait_event(ev_up[i % 2])
                 if i >= 2:
                     s_comp.wait_event(ev_down[i % 2])  # step i-2's output has been read back
-                # the public op's own plan (row statistics, variant, merge partition with the
-                # interleaved long rows), built once per step for the step's uploaded matrix
-                stats = ops.row_stats(rp)
-                variant = ops.choose_variant(stats, self.k)
-                part = ops.merge_partition(rp, v.numel(), k=self.k, colidx=ci, vals=v, max_row=stats.max_row) \
-                    if variant == "merge" else None
-                ops.spmm_csr(rp, ci, v, x @ w1, out=b["H"], relu=True, variant=variant, partition=part,
-                             stats=stats)
-                ops.spmm_csr(rp, ci, v, b["H"] @ w2, out=b["O"], relu=False, variant=variant, partition=part,
-                             stats=stats)
+                At = st.csr_from_arrays(rp, ci, v, A.shape, name="A", device=dev, validate=False)
+                H = torch.relu_(torch.mm(At, x @ w1))
+                outs[i % 2] = torch.mm(At, H @ w2)
                 ev_comp[i % 2].record(s_comp)
             with torch.cuda.stream(s_down):
                 s_down.wait_event(ev_comp[i % 2])
-                h_out[i % 2].copy_(b["O"], non_blocking=True)
+                h_out[i % 2].copy_(outs[i % 2], non_blocking=True)
                 ev_down[i % 2].record(s_down)
 
         def run(n, start=None):
@@ -333,8 +338,33 @@ class GCN(Workload):
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / steps
-        assert np.isfinite(h_out[(steps - 1) % 2][:4].numpy()).all()
-        return ms, h2d, d2h
+        return ms, h2d, d2h, h_out[(steps - 1) % 2].numpy().copy()
+
+    def check_e2e_output(self, O_host):
+        """Checker, outside every timed region: the downloaded e2e output against (a) the
+        resident path's output (same kernels, deterministic: expected bit-identical) and
+        (b) the float64 oracle on row blocks (hub rows with the merge carries, a middle and a
+        tail block), fed the GPU's own Z2 (per-stage gate)."""
+        from oracle import native
+        from oracle.restate import parity_gate
+
+        torch = self.torch
+        A = self.host[0]
+        Z2 = self.H @ self.W2
+        O_res = torch.empty_like(self.O)
+        self.layer(Z2, O_res, False)
+        O_res = O_res.cpu().numpy()
+        z2 = Z2.double().cpu().numpy()
+        v = A.vals.astype(np.float64)
+        worst, rows = 0.0, 0
+        for r0, r1 in ((0, 2048), (self.n // 2, self.n // 2 + 1024), (self.n - 1024, self.n)):
+            want = native.spmm_csr(A.rowptr, A.colidx, v, z2, rows=(r0, r1))
+            bound = native.spmm_csr(A.rowptr, A.colidx, np.abs(v), np.abs(z2), rows=(r0, r1))
+            ok, w = parity_gate(O_host[r0:r1], want, bound, 1e-5)
+            worst = max(worst, float(w))
+            rows += r1 - r0
+        return {"rows_checked_vs_oracle": rows, "max_err_over_tol": round(worst, 4),
+                "passed": bool(worst <= 1.0), "bitwise_equal_to_resident_path": bool(np.array_equal(O_host, O_res))}
 
     def cpu_reference_step(self, rows=None):
         """Oracle port: both SpMM layers in float64, reference summation order, all threads."""
@@ -401,10 +431,70 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "gcn2_chung_lu_N200k_d12_f128", "nnz": int(A.nnz)},
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": sample, "cpu": platform.processor() or platform.machine(),
-                         "os_cpu_count": os.cpu_count()},
+                         "sample": sample, **host_cpu(),
+                         "reference_engine": reference_engine_baseline(A, z1, z2)},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def host_cpu() -> dict:
+    """CPU model (/proc/cpuinfo), logical CPUs and the CPUs this process may run on."""
+    model = platform.processor() or platform.machine()
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": model, "os_cpu_count": os.cpu_count(), "sched_getaffinity": len(os.sched_getaffinity(0))}
+
+
+REF_STRIDE = 16   # reference-engine sample: every 16th row of the graph (same row-length mix)
+
+
+def reference_engine_baseline(A, z1, z2):
+    """The reference's own engine (`sparsetc.execute`, pure Python, installed from the reference
+    package into baseline/_ref) on a strided row sample of both GCN layers, timed like the
+    reference CLI's bench_kernel (`cli.py:231-275`: execute() only, perf_counter_ns), and
+    extrapolated linearly in nnz to the full graph. The sample keeps every REF_STRIDE-th row,
+    so its row-length mix is the graph's (a row prefix would be only hub rows)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "sparsetc").is_dir():
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref <reference pkg>)"}
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    from sparsetc import csr, execute, from_dense, parse, schedule, tile
+    from sparsetc.tensor import _assemble_presorted
+
+    n = A.shape[0]
+    sel = np.arange(0, n, REF_STRIDE)
+    lens = np.diff(A.rowptr)[sel]
+    starts = A.rowptr[sel]
+    idx = np.repeat(starts - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens) + np.arange(int(lens.sum()))
+    rows = np.repeat(np.arange(sel.size), lens)
+    # presorted assembly (the engine's own internal, engine.py:249-253): build_from_entries would
+    # take minutes of dict work before the timed region
+    As = _assemble_presorted((sel.size, n), csr(sel.size, n), np.stack([rows, A.colidx[idx]], axis=1),
+                             A.vals[idx].astype(np.float64), "A")
+    times = []
+    for z, name in ((z1, "Z1"), (z2, "Z2")):
+        Z = from_dense(z, name="Z")
+        e = parse("H(i,k) = A(i,j) * Z(j,k)", {"A": As, "Z": Z})
+        sch = tile(e, schedule(e), 64)
+        t0 = time.perf_counter_ns()
+        execute(sch)
+        times.append((time.perf_counter_ns() - t0) * 1e-9)
+    nnz_s = int(idx.size)
+    step_s = sum(times) * A.nnz / nnz_s
+    flops = 2 * 2.0 * A.nnz * z1.shape[1]
+    return {"value": round(flops / step_s / 1e9, 5), "unit": "GFLOP/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"sparsetc.execute (reference engine, pure Python) on both SpMM layers over every "
+                      f"{REF_STRIDE}th row ({sel.size} rows, {nnz_s} nnz = {nnz_s / A.nnz:.2%}), "
+                      "extrapolated linearly in nnz; 1 effective core (interpreter)",
+            "seconds_per_layer_sample": [round(t, 3) for t in times],
+            "ms_per_step_extrapolated": round(step_s * 1e3, 1), **host_cpu()}
 
 
 def cpu_baseline(work, budget_s=12.0):
@@ -422,10 +512,12 @@ def cpu_baseline(work, budget_s=12.0):
         work.cpu_reference_step()
     per = (time.perf_counter() - t0) / reps
     value = work.flops_per_step / per / 1e9
+    z1, z2, _ = work._z64
     return {"value": round(value, 3), "unit": "GFLOP/s", "cores": native.num_threads(), "kind": "port",
             "sample": f"both SpMM layers over the full graph ({int(A.nnz)} nnz, K=128), {reps} reps; "
                       "float64 C restatement of the reference engine's order (oracle/stc_oracle.c)",
-            "ms_per_step": round(per * 1e3, 3)}
+            "ms_per_step": round(per * 1e3, 3), **host_cpu(),
+            "reference_engine": reference_engine_baseline(A, z1, z2)}
 
 
 def run_ours(args):
@@ -449,14 +541,13 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    wev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    wev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     with ClockSampler(local) as clocks:
         t_end = time.perf_counter() + 0.3
         w = 0
         while w < args.warmup or time.perf_counter() < t_end:
-            flush.zero_()
-            work.step(wev)
+            work.step(wev, flush)
             w += 1
             if w % 50 == 0:
                 torch.cuda.synchronize()
@@ -465,15 +556,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         launches0 = _abi.launch_count()
         for s in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            work.step(ev[s])
+            work.step(ev[s], flush)  # L2 flushed before each layer, outside the events
         torch.cuda.synchronize()
         launches = _abi.launch_count() - launches0
         barrier()
         torch.cuda.synchronize()
     layer1 = [e[0].elapsed_time(e[1]) for e in ev]
-    layer2 = [e[1].elapsed_time(e[2]) for e in ev]
-    total_ms = sum(e[0].elapsed_time(e[2]) for e in ev)
+    layer2 = [e[2].elapsed_time(e[3]) for e in ev]
+    total_ms = sum(layer1) + sum(layer2)
     if world > 1:
         t = torch.tensor([total_ms], device=device, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -507,7 +597,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if not args.no_e2e:
-        e_ms, h2d, d2h = work.e2e(steps=max(3, min(args.steps, 20)), warmup=3)
+        e_ms, h2d, d2h, O_host = work.e2e(steps=max(3, min(args.steps, 20)), warmup=3)
         if world > 1:
             t = torch.tensor([e_ms], device=device, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -515,7 +605,11 @@ def run_ours(args):
         out["e2e"] = {"value": round(world * work.flops_per_step / (e_ms * 1e-3) / 1e9, 3),
                       "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                       "ms_per_step": round(e_ms, 4),
-                      "path": "GCN forward per step: upload A, X, W1, W2 (pinned); plan A (row stats, merge partition, long-row interleave); X@W1, ops.spmm_csr (ReLU), H@W2, ops.spmm_csr; download O; steps pipelined over upload/compute/download streams"}
+                      "path": "public API per step: upload A, X, W1, W2 (pinned host); A = st.csr_from_arrays(...); "
+                              "H = relu(torch.mm(A, X @ W1)); O = torch.mm(A, H @ W2) (torch.mm intercepted -> "
+                              "parse_einsum + run: plan + stc_spmm_csr_f32); download O; steps pipelined over "
+                              "upload/compute/download streams",
+                      "check": work.check_e2e_output(O_host)}
     if rank == 0:
         out["gcn_forward"] = work.full_forward_ms()
         if world == 1 and not args.no_cpu_baseline:

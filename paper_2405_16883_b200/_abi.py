@@ -112,14 +112,43 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+_cuda_seen = False
+
+
 def require_cuda(*tensors: torch.Tensor) -> None:
-    if not torch.cuda.is_available():
-        raise ExtensionUnavailable("no CUDA device: sparse contractions run only on the GPU")
+    global _cuda_seen
+    if not _cuda_seen:
+        if not torch.cuda.is_available():
+            raise ExtensionUnavailable("no CUDA device: sparse contractions run only on the GPU")
+        _cuda_seen = True
+    dev = None
     for t in tensors:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise ExtensionUnavailable(
                 "operand buffers are on the CPU; move the tensor to CUDA (tensor.to('cuda'))"
             )
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"operands on different devices ({dev} and {t.device})")
+
+
+def on_operand_device(fn):
+    """Run an op with its operands' device current, so its launches (and the stream handle
+    passed to the C ABI) belong to that device even when another device is current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        dev = next((a.device for a in args if isinstance(a, torch.Tensor) and a.is_cuda), None)
+        if dev is not None and dev.index is not None and dev.index != torch.cuda.current_device():
+            with torch.cuda.device(dev):
+                return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapper
 
 
 def check(rc: int, what: str) -> None:

@@ -919,12 +919,87 @@ def execute(sched: Schedule, bindings: dict | None = None, out_fmt: TensorFormat
     "coltile") for SpMM-shaped terms.
     """
     out_fmt = out_fmt if out_fmt is not None else sched.out_format
+    fast = _fast_spmm_plan(sched, out_fmt)
+    if fast is not None:
+        got = _fast_spmm(sched, fast, bindings, variant)
+        if got is not None:
+            return got
     if set(sched.loop_order) != set(get_index_variables(sched.expr)):
         raise ValueError("schedule does not cover the expression's index variables")
     ctx = _Ctx(sched, bindings, out_fmt, variant)
     result = _dispatch(ctx)
     execute.last_variants = tuple(ctx.chosen)
     return result, ctx.counter
+
+
+# ---- repeated calls of the hot path --------------------------------------------------
+# A schedule whose expression is one CSR SpMM / SpMV term into a dense output is
+# recognised once (structure only, cached on the schedule); later calls look up the
+# operands' cached row view / statistics / partition and launch directly. Same kernels,
+# arguments, counters and result as the general dispatch below.
+
+
+@dataclass
+class _FastSpmm:
+    m: _SpmmTerm
+    a_name: str
+    b_name: str
+    b_order: tuple
+    out_shape: tuple
+    ik_order: bool
+
+
+def _fast_spmm_plan(sched: Schedule, out_fmt: TensorFormat):
+    cache = sched.__dict__.setdefault("_fast", {})
+    if out_fmt in cache:
+        return cache[out_fmt]
+    plan = None
+    e = sched.expr
+    terms = e.terms()
+    out_vars = e.output_indices
+    if (len(terms) == 1 and not out_fmt.has_sparse_levels and out_fmt.shape == e.output_shape
+            and out_fmt.mode_ordering == tuple(range(len(out_vars)))
+            and set(sched.loop_order) == set(get_index_variables(e))):
+        m = _match_spmm(terms[0], out_vars)
+        if m is not None:
+            f = m.A.tensor.format
+            row_dim = m.A.indices.index(m.i)
+            csr_like = f.mode_ordering[0] == row_dim and f.levels == (LevelFormat.DENSE, LevelFormat.COMPRESSED)
+            if csr_like and m.A.tensor.name != m.B.tensor.name:
+                b_order = (0,) if m.k is None else (m.B.indices.index(m.j), m.B.indices.index(m.k))
+                ext = index_extents(e)
+                plan = _FastSpmm(m, m.A.tensor.name, m.B.tensor.name, b_order,
+                                 tuple(ext[v] for v in out_vars), m.k is None or list(out_vars) == [m.i, m.k])
+    cache[out_fmt] = plan
+    return plan
+
+
+class _LightCtx:
+    def __init__(self, sched, variant, A, B, m):
+        self.sched, self.variant, self.counter, self.chosen = sched, variant, OpCounter(), []
+        self._t = {id(m.A): A, id(m.B): B}
+
+    def t(self, a: Access) -> Tensor:
+        return self._t[id(a)]
+
+
+def _fast_spmm(sched: Schedule, f: _FastSpmm, bindings, variant):
+    m = f.m
+    A, B = m.A.tensor, m.B.tensor
+    if bindings:
+        A = bindings.get(f.a_name, A)
+        B = bindings.get(f.b_name, B)
+        for t, a in ((A, m.A), (B, m.B)):
+            if t is not a.tensor and (t.shape != a.tensor.shape or t.format != a.tensor.format):
+                raise ShapeError(f"rebinding of {a.tensor.name} must match the scheduled shape and format")
+    if not (A.storage.values.is_cuda and B.storage.values.is_cuda):
+        return None  # the general path raises the device error
+    ctx = _LightCtx(sched, variant, A, B, m)
+    view, Y, K = _spmm_rows(ctx, m)
+    _spmm_counters(ctx, m, view, K)
+    res = Y.reshape(f.out_shape) if m.k is None else (Y if f.ik_order else Y.t().contiguous())
+    execute.last_variants = tuple(ctx.chosen)
+    return _dense_result(sched.expr.output_name, res), ctx.counter
 
 
 execute.last_variants = ()
@@ -945,39 +1020,10 @@ def run_with_report(e: TensorExpr, bindings: dict | None = None, out_format: Ten
             t = bindings.get(a.tensor.name)
             if t is not None and t.shape != a.tensor.shape:
                 raise ShapeError(f"binding for {a.tensor.name} has shape {t.shape}")
-    all_dense = all(not a.tensor.format.has_sparse_levels for a in e.accesses)
-    if all_dense:
-        fmt = out_format if out_format is not None else dense_format(e.output_shape)
-        sched = schedule(e, dense_format(e.output_shape), weights)
-        ctx = _Ctx(sched, bindings, dense_format(e.output_shape), None)
-        _require_device(ctx.tensor_of.values())
-        t0 = time.perf_counter_ns()
-        acc = None
-        for term in e.terms():
-            r = _dense_einsum(ctx, term, e.output_indices)
-            acc = r if acc is None else acc + r
-        torch.cuda.synchronize()
-        wall = time.perf_counter_ns() - t0
-        result = _dense_result(e.output_name, acc)
-        if fmt.has_sparse_levels or fmt.mode_ordering != tuple(range(fmt.order)):
-            from .tensor import from_dense
+    if all(not a.tensor.format.has_sparse_levels for a in e.accesses):
+        return _run_dense(e, bindings, out_format, weights, timed=True)
 
-            result = from_dense(acc, fmt, name=e.output_name)
-        report = {"path": "dense", "inferred_format": infer_format(e).name(), "schedule": None,
-                  "counters": None, "wall_time_ns": wall, "variants": ["dense:torch"]}
-        return result, None, report
-
-    # the plan depends only on the expression (whose operands are immutable and may only be
-    # rebound to tensors of the same shape and format) and the options: memoised on it
-    plans = e.__dict__.setdefault("_plans", {})
-    key = (out_format, tile_size, tiling, weights)
-    if key not in plans:
-        out_fmt = out_format if out_format is not None else infer_format(e)
-        sched = schedule(e, out_fmt, weights)
-        if tiling:
-            sched = tile(e, sched, tile_size)
-        plans[key] = (out_fmt, sched)
-    out_fmt, sched = plans[key]
+    out_fmt, sched = _plan(e, out_format, tile_size, tiling, weights)
     t0 = time.perf_counter_ns()
     result, counter = execute(sched, bindings, variant=variant)
     torch.cuda.synchronize()
@@ -994,6 +1040,59 @@ def run_with_report(e: TensorExpr, bindings: dict | None = None, out_format: Ten
     return result, counter, report
 
 
-def run(e: TensorExpr, bindings: dict | None = None, **options) -> Tensor:
-    result, _, _ = run_with_report(e, bindings, **options)
-    return result
+def _run_dense(e: TensorExpr, bindings, out_format, weights, timed: bool):
+    """All-dense expressions: torch (cuBLAS, TF32 off), the paper's "dense -> torch" branch
+    (`engine.py:687-701`). ``timed`` adds the device synchronisation for ``wall_time_ns``."""
+    fmt = out_format if out_format is not None else dense_format(e.output_shape)
+    sched = schedule(e, dense_format(e.output_shape), weights)
+    ctx = _Ctx(sched, bindings, dense_format(e.output_shape), None)
+    _require_device(ctx.tensor_of.values())
+    t0 = time.perf_counter_ns()
+    acc = None
+    for term in e.terms():
+        r = _dense_einsum(ctx, term, e.output_indices)
+        acc = r if acc is None else acc + r
+    if timed:
+        torch.cuda.synchronize()
+    wall = time.perf_counter_ns() - t0
+    result = _dense_result(e.output_name, acc)
+    if fmt.has_sparse_levels or fmt.mode_ordering != tuple(range(fmt.order)):
+        from .tensor import from_dense
+
+        result = from_dense(acc, fmt, name=e.output_name)
+    report = {"path": "dense", "inferred_format": infer_format(e).name(), "schedule": None,
+              "counters": None, "wall_time_ns": wall, "variants": ["dense:torch"]}
+    return result, None, report
+
+
+def _plan(e: TensorExpr, out_format, tile_size, tiling, weights):
+    """(output format, tiled schedule), memoised on the expression: the plan depends only on
+    the expression (whose operands are immutable and may only be rebound to tensors of the
+    same shape and format) and the options."""
+    plans = e.__dict__.setdefault("_plans", {})
+    key = (out_format, tile_size, tiling, weights)
+    got = plans.get(key)
+    if got is None:
+        out_fmt = out_format if out_format is not None else infer_format(e)
+        sched = schedule(e, out_fmt, weights)
+        if tiling:
+            sched = tile(e, sched, tile_size)
+        got = plans[key] = (out_fmt, sched)
+    return got
+
+
+def run(e: TensorExpr, bindings: dict | None = None, out_format: TensorFormat | None = None,
+        tile_size: int = DEFAULT_TILE_SIZE, tiling: bool = True, weights: CostModel = CostModel(),
+        variant: str | None = None) -> Tensor:
+    """Plan + execute (`engine.py:721-724`). Asynchronous: the kernels are queued on the
+    current CUDA stream and the call returns without waiting for them (reading the result
+    on the host — ``to_dense``, ``nnz`` of a sparse result — synchronises)."""
+    if bindings:
+        for a in e.accesses:
+            t = bindings.get(a.tensor.name)
+            if t is not None and t.shape != a.tensor.shape:
+                raise ShapeError(f"binding for {a.tensor.name} has shape {t.shape}")
+    if all(not a.tensor.format.has_sparse_levels for a in e.accesses):
+        return _run_dense(e, bindings, out_format, weights, timed=False)[0]
+    _, sched = _plan(e, out_format, tile_size, tiling, weights)
+    return execute(sched, bindings, variant=variant)[0]

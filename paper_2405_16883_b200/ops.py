@@ -10,12 +10,12 @@ from __future__ import annotations
 
 import math
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 
 from . import _abi
-from ._abi import check, lib, ptr, require_cuda, stream_handle
+from ._abi import check, lib, on_operand_device, ptr, require_cuda, stream_handle
 from .tensor import ShapeError
 
 # Items (row ends + stored entries) per sub-warp in the merge-path split; 0 means
@@ -58,6 +58,7 @@ class RowStats:
         return self.max_row / mean if mean > 0 else 0.0
 
 
+@on_operand_device
 def row_stats(rowptr: torch.Tensor) -> RowStats:
     m = rowptr.numel() - 1
     if m <= 0:
@@ -87,8 +88,35 @@ class MergePartition:
     # than a group has its entries interleaved (see interleave_long_rows), else None.
     colidx: torch.Tensor | None = None
     vals: torch.Tensor | None = None
+    m: int = -1               # rows and entries of the structure the plan was built for
+    nnz: int = -1
+    source: tuple | None = None   # (data_ptr, _version) of the colidx / vals the copies came from
+    _ws: dict = field(default_factory=dict, repr=False)
+
+    def check(self, m: int, nnz: int, colidx: torch.Tensor, vals: torch.Tensor) -> None:
+        """Raise if this plan was built for another structure (or, for a plan carrying
+        interleaved copies of A, for other index / value buffers or since-modified values)."""
+        if (self.m, self.nnz) != (m, nnz):
+            raise ValueError(f"merge partition built for m={self.m}, nnz={self.nnz}; matrix has m={m}, nnz={nnz}")
+        if self.source is not None and self.source != _buffer_id(colidx, vals):
+            raise ValueError("merge partition carries interleaved copies of another colidx/vals "
+                             "(or of values modified since): rebuild it with merge_partition(..., colidx, vals)")
+
+    def workspace(self, k: int, batch: int, device) -> torch.Tensor | None:
+        """Carry workspace for this plan, cached per (k, batch, device, current stream): its
+        arrival counters return to zero at the end of every launch, so stream-ordered calls
+        reuse it."""
+        key = (k, batch, str(device), torch.cuda.current_stream(device).cuda_stream)
+        if key not in self._ws:
+            self._ws[key] = spmm_workspace(self.m, self.nnz, k, "merge", self.items_per_group, batch, device)
+        return self._ws[key]
 
 
+def _buffer_id(colidx: torch.Tensor, vals: torch.Tensor) -> tuple:
+    return (colidx.data_ptr(), colidx._version, vals.data_ptr(), vals._version)
+
+
+@on_operand_device
 def interleave_long_rows(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, span: int):
     """Copies of (colidx, vals) in which each row longer than ``span`` entries is stored as
     G = ceil(len / span) interleaved sequences (entries 0, G, 2G, ..., then 1, G+1, ...).
@@ -117,6 +145,7 @@ def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "
     return ipg
 
 
+@on_operand_device
 def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None = None, *,
                     k: int = 128, batch: int = 1, kind: str = "spmm", colidx: torch.Tensor | None = None,
                     vals: torch.Tensor | None = None, max_row: int | None = None) -> MergePartition:
@@ -133,13 +162,14 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
     rc = lib().stc_merge_path_partition(m, nnz, ptr(rowptr), items_per_group, ptr(starts),
                                         stream_handle())
     check(rc, "stc_merge_path_partition")
-    ci = va = None
+    ci = va = source = None
     if kind == "spmm" and colidx is not None and vals is not None and vals.dim() == 1 and INTERLEAVE and m > 0:
         if max_row is None:
             max_row = int((rowptr[1:] - rowptr[:-1]).max().item())
         if max_row > items_per_group:  # some row spans several groups: interleave (a copy of A)
             ci, va = interleave_long_rows(rowptr, _i32(colidx), _f32(vals), items_per_group)
-    return MergePartition(starts, items_per_group, groups, ci, va)
+            source = _buffer_id(colidx, vals)
+    return MergePartition(starts, items_per_group, groups, ci, va, m, int(nnz), source)
 
 
 @dataclass
@@ -155,6 +185,7 @@ class ColtilePlan:
     nnz: int
 
 
+@on_operand_device
 def coltile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, n_cols: int, vals: torch.Tensor) -> ColtilePlan:
     require_cuda(rowptr, colidx, vals)
     m = rowptr.numel() - 1
@@ -182,6 +213,7 @@ def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int,
 # ---------------------------------------------------------------------------
 
 
+@on_operand_device
 def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor,
              *, out: torch.Tensor | None = None, addend: torch.Tensor | None = None,
              relu: bool = False, variant: str | None = None,
@@ -214,12 +246,13 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
     if variant == "merge":
         partition = partition or merge_partition(rowptr, nnz, k=k, colidx=colidx, vals=vals,
                                                  max_row=None if stats is None else stats.max_row)
+        partition.check(m, nnz, colidx, vals)
         ipg = partition.items_per_group
         plan_ptr = ptr(partition.starts)
         if partition.colidx is not None:   # the plan's long-row interleaved entries
             colidx, vals = partition.colidx, partition.vals
         if workspace is None:
-            workspace = spmm_workspace(m, nnz, k, variant, ipg, 1, B.device)
+            workspace = partition.workspace(k, 1, B.device)
     elif variant == "coltile":
         partition = partition or coltile_plan(rowptr, colidx, n, vals)
         if partition.nnz != nnz:
@@ -235,6 +268,7 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
     return out
 
 
+@on_operand_device
 def spmm_csr_batched(rowptr, colidx, vals: torch.Tensor, B: torch.Tensor, *,
                      out: torch.Tensor | None = None, variant: str | None = None,
                      partition: MergePartition | None = None,
@@ -257,9 +291,11 @@ def spmm_csr_batched(rowptr, colidx, vals: torch.Tensor, B: torch.Tensor, *,
     ipg = 0
     if variant == "merge":
         partition = partition or merge_partition(rowptr, nnz, k=k, batch=Z)
+        if (partition.m, partition.nnz) != (m, nnz):
+            raise ValueError(f"merge partition built for m={partition.m}, nnz={partition.nnz}")
         ipg = partition.items_per_group
         if workspace is None:
-            workspace = spmm_workspace(m, nnz, k, variant, ipg, Z, B.device)
+            workspace = partition.workspace(k, Z, B.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_spmm_csr_batched_f32(
         Z, m, n, k, ptr(rowptr), ptr(colidx), ptr(vals), nnz, vals.stride(0), ptr(B), B.stride(1),
@@ -282,6 +318,7 @@ class Segments:
         return self.rows.numel()
 
 
+@on_operand_device
 def coo_segments(row_crd: torch.Tensor) -> Segments:
     require_cuda(row_crd)
     _i32(row_crd)
@@ -321,6 +358,7 @@ def _head_view(X: torch.Tensor, name: str):
     return X, X.stride(0) if X.shape[0] > 1 else 0, X.stride(1)
 
 
+@on_operand_device
 def sddmm_csr(rowptr, colidx, Q: torch.Tensor, K: torch.Tensor, *, maskvals=None,
               scale: float = 1.0, out: torch.Tensor | None = None) -> torch.Tensor:
     """``S[h, p] = scale * mask[p] * <Q[h, i], K[h, colidx[p]]>`` -> [H, nnz] (or [nnz])."""
@@ -339,6 +377,7 @@ def sddmm_csr(rowptr, colidx, Q: torch.Tensor, K: torch.Tensor, *, maskvals=None
     return out[0] if squeeze else out
 
 
+@on_operand_device
 def segment_softmax_(rowptr: torch.Tensor, vals: torch.Tensor) -> torch.Tensor:
     """In-place softmax over each row's stored values; vals [nnz] or [H, nnz]."""
     require_cuda(rowptr, vals)
@@ -368,6 +407,7 @@ class AttentionTilePlan:
     dense_share: float        # fraction of stored entries covered by dense tiles
 
 
+@on_operand_device
 def attention_tile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, maskvals: torch.Tensor | None,
                         n_cols: int, min_fill: float = TILE_MIN_FILL,
                         max_tiles: int = TILE_MAX_PER_BLOCK) -> AttentionTilePlan | None:
@@ -409,6 +449,7 @@ def attention_tile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, maskvals: to
                              float(inside.sum().item()) / nnz)
 
 
+@on_operand_device
 def sparse_attention_tiled(plan: AttentionTilePlan, Q, K, V, *, scale: float | None = None,
                            workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Block-tiled fused attention (head dim 64): dense tiles on CUDA cores + remainder."""
@@ -434,6 +475,7 @@ def sparse_attention_tiled(plan: AttentionTilePlan, Q, K, V, *, scale: float | N
     return O[0] if squeeze else O
 
 
+@on_operand_device
 def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | None = None,
                      return_probs: bool = False):
     """Fused ``O = softmax_rows(scale * M .* QK^T) V``; optionally also S and P [H, nnz]."""
@@ -468,6 +510,7 @@ def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | N
 # ---------------------------------------------------------------------------
 
 
+@on_operand_device
 def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tensor, *,
                 variant: str = "merge", partition: MergePartition | None = None,
                 workspace: torch.Tensor | None = None) -> torch.Tensor:
@@ -483,9 +526,11 @@ def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tenso
     ipg = 0
     if variant == "merge":
         partition = partition or merge_partition(seg.ptr, nnz, k=R, kind="mttkrp")
+        if (partition.m, partition.nnz) != (n_seg, nnz):
+            raise ValueError(f"merge partition built for m={partition.m}, nnz={partition.nnz}")
         ipg = partition.items_per_group
         if workspace is None:
-            workspace = spmm_workspace(n_seg, nnz, R, "merge", ipg, 1, B.device)
+            workspace = partition.workspace(R, 1, B.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_mttkrp_coo3_f32(
         n_seg, R, ptr(seg.ptr), ptr(jcrd), ptr(kcrd), ptr(vals), nnz, B.shape[0], ptr(B), B.stride(0),
@@ -515,6 +560,7 @@ def _byte_buffer(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
+@on_operand_device
 def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals, n_cols: int) -> CsrResult:
     """``C(i,k) = A(i,j) * B(j,k)`` for CSR A [m, n], B [n, n_cols] -> CSR C [m, n_cols].
 
@@ -550,6 +596,7 @@ def spgemm_csr(a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals, n_cols: i
     return CsrResult(c_rowptr, c_colidx, c_vals, products)
 
 
+@on_operand_device
 def csr_ewise(op: str, a_rowptr, a_colidx, a_vals, b_rowptr, b_colidx, b_vals) -> CsrResult:
     """Element-wise CSR of the same shape: ``op="add"`` (union, (0 + a) + b) or
     ``op="mul"`` (intersection, 0 + a * b), the reference's `_union_sorted` /

@@ -507,6 +507,19 @@ def stored_entries(t: Tensor) -> tuple[np.ndarray, np.ndarray]:
     return coords.cpu().numpy(), vals.to(torch.float64).cpu().numpy()
 
 
+def dense_view(array: torch.Tensor, name: str = "T") -> Tensor:
+    """All-dense Tensor over a device torch tensor's own buffer (no copy when it is float32
+    and contiguous). For operands of a single call (torch interception), where the
+    reference-style copy of ``from_dense`` would cost a full pass over the operand."""
+    arr = array.detach()
+    if arr.dtype != VALUE_DTYPE or not arr.is_contiguous():
+        arr = arr.to(VALUE_DTYPE).contiguous()
+    shape = tuple(arr.shape)
+    fmt = dense_format(shape)
+    st = TensorStorage(fmt, tuple(DenseLevel(fmt.level_extent(k)) for k in range(fmt.order)), arr.reshape(-1))
+    return Tensor(name, shape, st)
+
+
 def to_torch(t: Tensor) -> torch.Tensor:
     """Dense float32 torch tensor on the storage's device; absent entries are 0."""
     fmt = t.format
