@@ -10,6 +10,7 @@ There is no fallback: if the library or a GPU is missing, ``lib()`` raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -17,7 +18,8 @@ import torch
 
 from .tensor import ShapeError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libstc.so"
+# STC_LIBRARY selects another build of the same ABI (the checked build, tools/run_checked.sh)
+_LIB_PATH = Path(os.environ.get("STC_LIBRARY") or Path(__file__).resolve().parent / "libstc.so")
 _lock = threading.Lock()
 _lib = None
 

@@ -14,6 +14,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libstc.so"
+# checked build: device-side bounds / protocol checks (STC_CHECK) compiled in; for test runs
+# only (tools/run_checked.sh loads it through STC_LIBRARY)
+LIB_CHECKED = PKG / "libstc_checked.so"
 SOURCES = ["abi_common.cu", "spmm.cu", "spmm_wide.cu", "attention.cu", "spgemm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -27,23 +30,26 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_build() -> bool:
-    if not LIB.exists():
+def needs_build(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    mtime = LIB.stat().st_mtime
+    mtime = lib.stat().st_mtime
     deps = list(CSRC.glob("*")) + [PKG.parent / "include" / "stc.h"]
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    """Compile every .cu to an object, link ``libstc.so``; returns its path."""
-    if not force and not needs_build():
-        return LIB
+def build(verbose: bool = False, force: bool = False, checked: bool = False) -> Path:
+    """Compile every .cu to an object, link ``libstc.so`` (``libstc_checked.so`` with
+    ``checked``: STC_CHECKED defined); returns its path."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not needs_build(lib):
+        return lib
     nvcc = _nvcc()
-    build_dir = PKG / "build"
+    build_dir = PKG / ("build_checked" if checked else "build")
     build_dir.mkdir(exist_ok=True)
     objs = [str(build_dir / (Path(src).stem + ".o")) for src in SOURCES]
-    cmds = [[nvcc, *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", obj]
+    defs = ["-DSTC_CHECKED"] if checked else []
+    cmds = [[nvcc, *ARCH, *FLAGS, *defs, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src), "-o", obj]
             for src, obj in zip(SOURCES, objs)]
     # the translation units are independent: compile them concurrently
     procs = [subprocess.Popen(c, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for c in cmds]
@@ -57,16 +63,15 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             sys.stderr.write(err)
     if failed:
         raise RuntimeError(f"nvcc failed on {failed}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, force=True, checked="--checked" in sys.argv))

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
     for (int t = 0; t < G; ++t) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
+      STC_CHECK(t >= n || (c >= 0 && c < a.n), "SDDMM column outside K");
       if (t < n) kv = ld_gather4(Kh + (long long)c * a.k_rs);
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
       vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      STC_CHECK(t >= n || (c >= 0 && c < a.n), "attention column outside K/V");
       if (t < n) {
         kv = ld_gather4(Kh + (long long)c * a.k_rs);
         vv[t] = ld_gather4(Vh + (long long)c * a.v_rs);

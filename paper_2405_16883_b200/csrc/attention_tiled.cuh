@@ -16,12 +16,15 @@
 // remainder entries with the same online softmax and normalises.
 #pragma once
 
+#include <type_traits>
+
 #include "stc_common.cuh"
 
 namespace stc {
 
 constexpr int AT_B = 64;          // rows per block, columns per tile
 constexpr int AT_D = 64;          // head dim of the tiled path
+constexpr int AT_ABSENT = 0x7fc0ffee;  // score bits of an absent slot (a quiet NaN no FP op produces)
 
 struct TileArgs {
   int m, n, heads, n_blocks, dt_max;
@@ -89,6 +92,7 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
   };
   int n_t = 0;
   while (n_t < a.dt_max && cols[n_t] >= 0) ++n_t;
+  for (int t = 0; t < n_t; ++t) STC_CHECK(cols[t] * AT_B < a.n, "dense tile outside the key range");
   stage_rows(Qs, Qh, a.q_rs, row0, a.m, false);
   if (n_t > 0) {
     stage_rows(Ks, Kh, a.k_rs, cols[0] * AT_B, a.n, true);
@@ -147,7 +151,9 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
       float tmax = -INFINITY;
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        s[i][j] = isnan(mva[j]) ? -INFINITY : s[i][j] * mva[j] * a.scale;
+        // absent slot -> a NaN with a private payload (fmaxf skips it; below it becomes
+        // p = -0.0, "no entry"); a present entry's NaN score stays NaN, as in the reference
+        s[i][j] = isnan(mva[j]) ? __int_as_float(AT_ABSENT) : s[i][j] * mva[j] * a.scale;
         tmax = fmaxf(tmax, s[i][j]);
       }
 #pragma unroll
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
       float rsum = 0.f;
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        s[i][j] = (s[i][j] == -INFINITY) ? 0.f : expf(s[i][j] - mnew);
+        s[i][j] = __float_as_int(s[i][j]) == AT_ABSENT ? -0.f : ((s[i][j] == -INFINITY) ? 0.f : expf(s[i][j] - mnew));
         rsum += s[i][j];
       }
 #pragma unroll
@@ -177,24 +183,43 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
           make_float4(s[4][j], s[5][j], s[6][j], s[7][j]);
     }
     cp_async_wait<0>();  // V(t) landed
-    __syncthreads();
-#pragma unroll 2
-    for (int c = 0; c < AT_B; ++c) {
-      const int sw = (c >> 2) & 7;
-      const float4 pa = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ sw));
-      const float4 pb = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw));
-      const float p8[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-      float v8[CW];
-#pragma unroll
-      for (int eq = 0; eq < CW / 4; ++eq) {
-        const float4 v4 = *reinterpret_cast<const float4*>(Vs + c * AT_D + at8_col<TXN>(tx, 4 * eq));
-        v8[4 * eq] = v4.x; v8[4 * eq + 1] = v4.y; v8[4 * eq + 2] = v4.z; v8[4 * eq + 3] = v4.w;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int e = 0; e < CW; ++e) o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
+    // Absent slots carry p = -0.0: with finite V rows their products add nothing, but 0 * Inf
+    // would be NaN where the reference multiplies only stored entries. Each thread checks the
+    // V chunks it staged; if any row of the tile is not finite, the PV loop skips absent slots.
+    bool vfin = true;
+    for (int idx = tid; idx < AT_B * 16; idx += NT) {
+      const float4 v4 = *reinterpret_cast<const float4*>(Vs + (idx / 16) * AT_D + (idx % 16) * 4);
+      vfin &= isfinite(v4.x) && isfinite(v4.y) && isfinite(v4.z) && isfinite(v4.w);
     }
+    const bool v_finite = __syncthreads_and(vfin);
+    auto pv = [&](auto masked) {
+#pragma unroll 2
+      for (int c = 0; c < AT_B; ++c) {
+        const int sw = (c >> 2) & 7;
+        const float4 pa = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * (ty ^ sw));
+        const float4 pb = *reinterpret_cast<const float4*>(Pt + c * AT_B + 4 * ((8 + ty) ^ sw));
+        const float p8[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+        float v8[CW];
+#pragma unroll
+        for (int eq = 0; eq < CW / 4; ++eq) {
+          const float4 v4 = *reinterpret_cast<const float4*>(Vs + c * AT_D + at8_col<TXN>(tx, 4 * eq));
+          v8[4 * eq] = v4.x; v8[4 * eq + 1] = v4.y; v8[4 * eq + 2] = v4.z; v8[4 * eq + 3] = v4.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int e = 0; e < CW; ++e) {
+            if constexpr (decltype(masked)::value)
+              o[i][e] = signbit(p8[i]) ? o[i][e] : fmaf(p8[i], v8[e], o[i][e]);
+            else
+              o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
+          }
+      }
+    };
+    if (v_finite)
+      pv(std::false_type{});
+    else
+      pv(std::true_type{});
     __syncthreads();  // done with Vs and Pt: stream in the next tile's K and V
     if (t + 1 < n_t) {
       stage_rows(Ks, Kh, a.k_rs, cols[t + 1] * AT_B, a.n, true);

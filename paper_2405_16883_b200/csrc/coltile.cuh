@@ -29,6 +29,8 @@
 //   warps            consume chunk c, then a named barrier per quarter (4 warps)
 #pragma once
 
+#include <type_traits>
+
 #include "stc_common.cuh"
 
 namespace stc {
@@ -42,6 +44,7 @@ constexpr int CTT_STAGES = 3;
 constexpr int CTT_RPW = CTT_ROWS / CTT_WARPS;     // rows per consumer warp
 constexpr int CTT_PAD = 4;                        // row segments padded to this many entries
 constexpr int CTT_ECAP = 128;                     // staged entries per warp and chunk
+constexpr int CTT_PAD_ADDR = -1;                  // TMEM address of a padding entry
 constexpr size_t CTT_STAGE_FLOATS = (size_t)CTT_CHUNK * CTT_COLS;
 constexpr size_t CTT_SMEM = CTT_STAGES * CTT_STAGE_FLOATS * sizeof(float)  // B stages
                             + (size_t)CTT_WARPS * 2 * CTT_ECAP * 8          // entry lists (double)
@@ -114,7 +117,9 @@ __global__ void ctt_scatter_kernel(int m, int n_chunks, const int* __restrict__ 
     // lane quarter of the row's consumer warp, TMEM buffer of the chunk, 4 columns per B row
     const int base = ((32 * (((row % CTT_ROWS) / CTT_RPW) % 4)) << 16) + (c & 1) * 4 * CTT_CHUNK;
     for (int p = a; p < b; ++p) ent[e++] = make_int2(base + 4 * (colidx[p] - c * CTT_CHUNK), __float_as_int(vals[p]));
-    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(base, 0);
+    // padding: address -1 marks "no entry" (only a row's last group of 4 holds any; the
+    // kernel skips them there, so 0 * Inf / NaN from an unreferenced B row cannot occur)
+    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(CTT_PAD_ADDR, 0);
   }
 }
 
@@ -149,9 +154,10 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = *tbase_s;
-  // all 512 columns are allocated, so the allocation starts at lane 0, column 0: the plan's
-  // entries carry absolute TMEM addresses (no per-load address add in the inner loop)
-  if (tbase != 0u) __trap();
+  // all 512 columns are allocated (the allocation waits until the SM's TMEM is free), so it
+  // starts at lane 0, column 0: the plan's entries carry absolute TMEM addresses (no
+  // per-load address add in the inner loop)
+  STC_CHECK(tbase == 0u, "TMEM allocation does not start at column 0");
 
   if (warp == CTT_WARPS) {
     // ---------------- producer: B chunks -> SMEM stages (bulk copies, one per B row) ----------------
@@ -175,6 +181,7 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * row_bytes)
                      : "memory");
       __syncwarp();
+      STC_CHECK(j0 + rows <= n && c0 + row_bytes / 4 <= k, "B chunk outside the operand");
       for (int jr = lane; jr < rows; jr += 32)  // the warp's lanes issue the row copies in parallel
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -251,10 +258,22 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
     float acc[CTT_RPW][4];
 #pragma unroll
     for (int r = 0; r < CTT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
-    // 4 entries -> 4 tcgen05.ld, one wait, 16 FFMA
-    auto group = [&](float (&a)[4], int4 e01, int4 e23) {
+    // 4 entries -> 4 tcgen05.ld, one wait, 16 FFMA. TAIL: a row's last group, whose padding
+    // entries (address CTT_PAD_ADDR) load a valid address and leave the accumulators alone.
+    auto group = [&](float (&a)[4], int4 e01, int4 e23, auto tail) {
+      constexpr bool TAIL = decltype(tail)::value;
       uint32_t x[4][4];
-      const int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
+      int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
+      bool pad[4] = {false, false, false, false};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if constexpr (TAIL) {
+          pad[u] = taddr[u] == CTT_PAD_ADDR;
+          taddr[u] = pad[u] ? (int)tq : taddr[u];
+        }
+        STC_CHECK((uint32_t)taddr[u] >> 16 == 32u * quarter && (taddr[u] & 0xffff) < 512,
+                  "COLTILE entry outside the warp's TMEM lane quarter");
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
@@ -265,12 +284,15 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
                           __int_as_float(e23.w)};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        if (TAIL && pad[u]) continue;
         a[0] = fmaf(w[u], __uint_as_float(x[u][0]), a[0]);
         a[1] = fmaf(w[u], __uint_as_float(x[u][1]), a[1]);
         a[2] = fmaf(w[u], __uint_as_float(x[u][2]), a[2]);
         a[3] = fmaf(w[u], __uint_as_float(x[u][3]), a[3]);
       }
     };
+    using Body = std::false_type;
+    using Tail = std::true_type;
 
     int meta = load_meta(0);
     int meta_next = load_meta(1);
@@ -299,7 +321,11 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
           fill_step(r);
-          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], sc[q / 2], sc[q / 2 + 1]);
+          STC_CHECK(qa <= qb && qb <= total, "COLTILE row list outside the staged chunk list");
+          if (qb > qa) {
+            for (int q = qa; q < qb - CTT_PAD; q += CTT_PAD) group(acc[r], sc[q / 2], sc[q / 2 + 1], Body{});
+            group(acc[r], sc[(qb - CTT_PAD) / 2], sc[(qb - CTT_PAD) / 2 + 1], Tail{});
+          }
         }
       } else {  // rows denser than the staged list: entries straight from global memory
         const int4* g = reinterpret_cast<const int4*>(ent + e0);
@@ -308,7 +334,10 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
           const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
           const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
           fill_step(r);
-          for (int q = qa; q < qb; q += CTT_PAD) group(acc[r], g[q / 2], g[q / 2 + 1]);
+          if (qb > qa) {
+            for (int q = qa; q < qb - CTT_PAD; q += CTT_PAD) group(acc[r], g[q / 2], g[q / 2 + 1], Body{});
+            group(acc[r], g[(qb - CTT_PAD) / 2], g[(qb - CTT_PAD) / 2 + 1], Tail{});
+          }
         }
       }
       if (next) {

@@ -55,6 +55,7 @@ struct SpmmOp {
   const float* B;     // dense operand, row-major with leading dim ldb
   long long ldb;
   unsigned lane_off = 0;  // this lane's first column (added in 32-bit)
+  unsigned long long limit = ~0ull;  // elements of B (checked build: every gather stays inside)
 
   static constexpr int kRing = 8;           // gathers in flight per group
   static constexpr bool kHoistItem = true;  // next fetch's item read one step ahead
@@ -82,7 +83,10 @@ struct SpmmOp {
     return Item{__shfl_sync(mask, it.off, src, SUBW), __shfl_sync(mask, it.v, src, SUBW)};
   }
   STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
-  STC_DEVICE void fetch(const Item& it, Pre& pre) const { pre.b.load_gather(B + (it.off + lane_off)); }
+  STC_DEVICE void fetch(const Item& it, Pre& pre) const {
+    STC_CHECK((unsigned long long)(it.off + lane_off) + VEC <= limit, "SpMM gather outside B");
+    pre.b.load_gather(B + (it.off + lane_off));
+  }
   STC_DEVICE void accumulate(Frag<VEC>& acc, State&, const Pre& pre, const Item& it) const {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v, pre.b.v[e], acc.v[e]);
@@ -101,6 +105,7 @@ struct MttkrpOp {
   const float* C;
   long long ldcf;
   unsigned lane_off = 0;
+  unsigned long long limitb = ~0ull, limitc = ~0ull;  // elements of B / C (checked build)
 
   // Fiber factorisation: entries are sorted by (i, j), so consecutive entries of
   // one (i, j) fiber share B[j,:]. M[i,:] += B[j,:] * sum_k T[i,j,k] C[k,:] gathers
@@ -136,6 +141,8 @@ struct MttkrpOp {
   }
   STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
+    STC_CHECK(!it.flag || (unsigned long long)(it.offb + lane_off) + VEC <= limitb, "MTTKRP gather outside B");
+    STC_CHECK((unsigned long long)(it.offc + lane_off) + VEC <= limitc, "MTTKRP gather outside C");
     if (it.flag) pre.b.load_gather(B + (it.offb + lane_off));
     pre.c.load_gather(C + (it.offc + lane_off));
   }
@@ -214,6 +221,7 @@ struct SegOut {
 
 template <int VEC, int EPI, bool ADD>
 STC_DEVICE void write_row(const SegOut& o, int row, int col0, Frag<VEC> acc) {
+  STC_CHECK(row >= 0 && row < o.m && col0 + VEC <= o.k, "output row outside C");
   float* dst = o.C + (long long)row * o.ldc + col0;
   if constexpr (ADD) {
     Frag<VEC> d;
@@ -387,6 +395,8 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   const int row0 = s.x;
   const int n_rows = e.x - s.x;   // rows whose end item this group owns
   const int n_nnz = e.y - s.y;    // entries this group accumulates
+  STC_CHECK(n_rows >= 0 && n_nnz >= 0 && e.x <= o.m && n_nnz <= ms.ipg && n_rows <= ms.ipg,
+            "merge partition: group range");
 #ifdef STC_DBG_TIMING
   const unsigned long long t_start = dbg_timer();
 #endif
@@ -395,8 +405,10 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   int rb = 0;
   auto stage_rows = [&](int base) {
     __syncwarp(mask);
-    for (int t = lane; t < CAPR && base + t < n_rows; t += SUBW)
+    for (int t = lane; t < CAPR && base + t < n_rows; t += SUBW) {
       rend[t] = ld_stream(o.rowptr + row0 + base + 1 + t) - s.y;
+      STC_CHECK(rend[t] >= 0 && rend[t] <= n_nnz, "row end outside the group's entries");
+    }
     __syncwarp(mask);
   };
   stage_rows(0);
@@ -439,6 +451,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   typename Op::Pre ring[U];
   for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
     const int wn = min(CAP, n_nnz - w0);
+    STC_CHECK(wn + kStagePad <= IST, "staging window overflows its stride");
     __syncwarp(mask);
     // SU loads per lane in flight before their SMEM stores (one latency per SU * SUBW items)
     constexpr int SU = Op::kStageUnroll;
@@ -572,6 +585,7 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     auto arrive = [&](int r, int c_last) {
       const int c_first = (int)(((long long)kEntryCost * o.rowptr[r] + (long long)kRowCost * r) / ci);
       const int need = c_last - c_first + 1;
+      STC_CHECK(c_first >= 0 && c_first <= c_last && c_last < ms.n_cta, "carry chain outside the grid");
       int* ctr = ms.counters + zslab + c_last;
       if (atomicAdd(ctr, 1) + 1 == need) {
         *ctr = 0;  // every participant has arrived: reset for the next launch

@@ -165,6 +165,7 @@ __global__ void spgemm_dense_kernel(int phase, int m, int p, const int* __restri
       const float a = av[q];
       for (int t = bp[j] + lane; t < bp[j + 1]; t += 32) {
         const int k = bj[t];
+        STC_CHECK(k >= 0 && k < p, "SpGEMM column outside the dense window");
         atomicOr(&bits[k >> 5], 1u << (k & 31));
         if (phase == 1) acc[k] += a * bv[t];
       }
@@ -196,6 +197,7 @@ __global__ void spgemm_dense_kernel(int phase, int m, int p, const int* __restri
           const int bit = __ffs(b) - 1;
           b &= b - 1;
           const int k = w * 32 + bit;
+          STC_CHECK(o < cp[row + 1], "SpGEMM row overflows its counted length");
           ck[o] = k;
           cv[o] = acc[k];
           acc[k] = 0.0f;

@@ -116,9 +116,11 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
   if (wide) return spmm_wide(vec4 ? 4 : 1, epilogue, D != nullptr, o, ms, colidx, vals, B, ldb, L);
   if (vec4) {
     SpmmOp<4> op{colidx, vals, B, ldb};
+    op.limit = (unsigned long long)n * ldb;
     return dispatch_spmm<4>(epilogue, D != nullptr, o, ms, op, L);
   }
   SpmmOp<1> op{colidx, vals, B, ldb};
+  op.limit = (unsigned long long)n * ldb;
   return dispatch_spmm<1>(epilogue, D != nullptr, o, ms, op, L);
 }
 
@@ -407,9 +409,13 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   if (wide) return mttkrp_wide(vec, o, ms, jcrd, kcrd, vals, B, ldb, C, ldcf, subw, L);
   if (vec4) {
     MttkrpOp<4> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
+    op.limitb = (unsigned long long)n_j * ldb;
+    op.limitc = (unsigned long long)n_k * ldcf;
     return dispatch_subw<4, EPI_NONE, false>(subw, o, ms, op, L);
   }
   MttkrpOp<1> op{jcrd, kcrd, vals, B, ldb, C, ldcf};
+  op.limitb = (unsigned long long)n_j * ldb;
+  op.limitc = (unsigned long long)n_k * ldcf;
   return dispatch_subw<1, EPI_NONE, false>(subw, o, ms, op, L);
 }
 

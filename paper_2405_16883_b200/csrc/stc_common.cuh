@@ -13,6 +13,25 @@
 
 #define STC_DEVICE __device__ __forceinline__
 
+// Device-side bounds / protocol checks, compiled in only for the checked build
+// (libstc_checked.so, `python -m paper_2405_16883_b200._build --checked`; tools/run_checked.sh).
+// A failed check prints its site and traps, so the launch reports an error.
+#include <cstdio>
+#ifdef STC_CHECKED
+#define STC_CHECK(cond, what)                                                                        \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("STC_CHECK failed: %s (%s:%d) block (%d,%d,%d) thread %d\n", what, __FILE__, __LINE__,   \
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                                        \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define STC_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 namespace stc {
 
 constexpr int kWarp = 32;

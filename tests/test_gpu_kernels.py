@@ -349,3 +349,89 @@ def test_merge_with_interleaved_plan_matches_oracle():
     assert np.array_equal(got, again)  # fixed order: bit-reproducible
     want = native.spmm_csr(rp, ci, v, B)
     assert parity_gate(got, want, native.spmm_csr(rp, ci, np.abs(v), np.abs(B)), TOL)[0]
+
+
+# ---- non-finite values in operand rows no stored entry references ---------------
+
+def test_coltile_padding_ignores_nonfinite_unreferenced_rows():
+    """COLTILE pads each row's entries per 64-column chunk to a multiple of 4; the padding must
+    contribute nothing even when a B row of that chunk that the row never references holds
+    Inf / NaN (the reference multiplies stored entries only)."""
+    rng = np.random.default_rng(41)
+    m, n, k = 256, 256, 128
+    lens = rng.integers(1, 7, m)                      # rows need padding in most chunks
+    rp, ci, v = make_csr(rng, m, n, lens)
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    used = np.zeros(n, bool)
+    used[ci] = True
+    bad = np.flatnonzero(~used)
+    assert bad.size > 0
+    B[bad[0::2]] = np.inf
+    B[bad[1::2]] = np.nan
+    R, C, V = dev(rp, ci, v)
+    for variant in ("coltile", "merge", "row"):
+        got = ops.spmm_csr(R, C, V, torch.from_numpy(B).cuda(), variant=variant).cpu().numpy()
+        assert np.isfinite(got).all(), variant
+        want = native.spmm_csr(rp, ci, v, np.nan_to_num(B, nan=0, posinf=0))
+        bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(np.nan_to_num(B, nan=0, posinf=0)))
+        assert parity_gate(got, want, bound, TOL)[0], variant
+    # a referenced Inf still propagates like the reference (w * Inf, or 0 * Inf = NaN)
+    B2 = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    B2[ci[0]] = np.inf
+    got = ops.spmm_csr(R, C, V, torch.from_numpy(B2).cuda(), variant="coltile").cpu().numpy()
+    want = native.spmm_csr(rp, ci, v, B2)
+    assert np.array_equal(np.isnan(got), np.isnan(want)) and np.array_equal(np.isinf(got), np.isinf(want))
+
+
+def test_tiled_attention_ignores_nonfinite_unreferenced_value_rows():
+    """Dense 64x64 tiles hold absent slots; a V row that some rows of the block do not
+    reference may be Inf / NaN without touching those rows (rows that reference it do)."""
+    from paper_2405_16883_b200 import synthetic
+
+    M, Q, K, V = synthetic.cfg4(seq=256, heads=1, dim=64, window=48, n_random=4)
+    R, Cc, MV = dev(M.rowptr, M.colidx, M.vals)
+    plan = ops.attention_tile_plan(R, Cc, MV, 256)
+    assert plan is not None
+    bad = 100
+    V = V.copy()
+    V[0, bad] = np.inf
+    Qt, Kt, Vt = (torch.from_numpy(x).cuda() for x in (Q, K, V))
+    O = ops.sparse_attention_tiled(plan, Qt, Kt, Vt, scale=0.125).cpu().numpy()[0]
+    refs = np.zeros(M.shape[0], bool)
+    rows = np.repeat(np.arange(M.shape[0]), np.diff(M.rowptr))
+    refs[rows[M.colidx == bad]] = True
+    assert np.isfinite(O[~refs]).all()
+    s = 0.125 * native.sddmm_csr(M.rowptr, M.colidx, M.vals, Q[0], K[0])
+    p = native.segment_softmax(M.rowptr, s)
+    o = native.spmm_csr(M.rowptr, M.colidx, p, V[0])
+    ob = native.spmm_csr(M.rowptr, M.colidx, p, np.abs(np.nan_to_num(V[0], posinf=0)))
+    keep = ~refs
+    assert parity_gate(O[keep], o[keep], ob[keep], TOL)[0]
+    assert np.array_equal(np.isfinite(O[refs]), np.isfinite(o[refs]))
+
+
+# ---- cross-CTA carry protocol under repetition ------------------------------------------------
+
+@pytest.mark.parametrize("ipg", [1, 2, 5])
+def test_merge_carries_bitwise_stable_over_many_launches(ipg):
+    """Rows cut across many CTAs (items per group 1..5): the last-arriving CTA combines the
+    carries in position order. 300 back-to-back launches (different CTA arrival orders) must
+    all be bit-identical and match the oracle; the arrival counters must return to zero."""
+    rng = np.random.default_rng(ipg)
+    lens = np.where(np.arange(64) % 9 == 0, 700, rng.integers(0, 5, 64))
+    rp, ci, v = make_csr(rng, 64, 800, lens)
+    R, C, V = dev(rp, ci, v)
+    B = torch.randn(800, 64, device="cuda")
+    part = ops.merge_partition(R, len(v), ipg)
+    ws = ops.spmm_workspace(64, len(v), 64, "merge", part.items_per_group, 1, "cuda")
+    first = ops.spmm_csr(R, C, V, B, variant="merge", partition=part, workspace=ws, relu=True)
+    outs = [ops.spmm_csr(R, C, V, B, variant="merge", partition=part, workspace=ws, relu=True) for _ in range(300)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(first, o) for o in outs)
+    # workspace = head partials | tail partials (n_cta x 64 floats each) | n_cta arrival counters
+    n_cta = -(-part.n_groups // 16)  # k = 64: 16-lane groups, 16 per CTA
+    counters = ws.view(torch.int32)[2 * n_cta * 64: 2 * n_cta * 64 + n_cta]
+    assert int(counters.abs().sum()) == 0
+    want = native.spmm_csr(rp, ci, v, B.cpu().numpy().astype(np.float64), relu=True)
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B.cpu().numpy().astype(np.float64)))
+    assert parity_gate(first.cpu().numpy(), want, bound, TOL)[0]
