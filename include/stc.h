@@ -186,8 +186,8 @@ int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, int n_blocks,
                                    long long o_rs, void* ws, size_t ws_bytes, void* stream);
 
 /* MTTKRP over a sorted COO 3-tensor, segmented by distinct i:
- * M[s,:] = sum_{p in seg s} vals[p] * B[j[p],:] * C[k[p],:], evaluated fiber by
- * fiber: each run of equal j sums vals * C[k,:] and multiplies by B[j,:] once.
+ * M[s,:] = sum_{p in seg s} (vals[p] * B[j[p],:]) * C[k[p],:], terms added in entry
+ * order; B[j,:] is gathered once per run of equal j (an (i, j) fiber).
  * B has n_j rows, C has n_k rows (below 2^32 elements the gathers use prepared 32-bit
  * offsets, at or above it 64-bit addresses; any size that fits in memory).
  * Replaces `_run_sparse_output` with the (i,r) Workspace, engine.py:577-644,

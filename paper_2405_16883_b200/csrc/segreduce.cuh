@@ -107,14 +107,24 @@ struct MttkrpOp {
   unsigned lane_off = 0;
   unsigned long long limitb = ~0ull, limitc = ~0ull;  // elements of B / C (checked build)
 
-  // Fiber factorisation: entries are sorted by (i, j), so consecutive entries of
-  // one (i, j) fiber share B[j,:]. M[i,:] += B[j,:] * sum_k T[i,j,k] C[k,:] gathers
-  // B[j,:] once per fiber (flag = first entry of a fiber) instead of once per entry.
+  // Entries are sorted by (i, j), so consecutive entries of one (i, j) fiber share
+  // B[j,:]: it is gathered once per fiber (flag = first entry of a fiber) and held in
+  // registers, and every entry adds its term (T * B[j,:]) * C[k,:] in entry order (the
+  // reference's term order, engine.py:577-644) -- 3 ops per element. (The fiber-sum form
+  // B[j,:] * sum_k T C[k,:] costs 5 ops per element with its open/close selects: cfg5
+  // 135 -> 131 us; its loop alone 68 -> 53 us in a diagnostic build without gathers.)
   static constexpr int kRing = VEC == 4 ? 4 : 8;
   static constexpr bool kHoistItem = false;
-  static constexpr int kMinBlocks = 3;
+#ifndef STC_MTTKRP_MINB
+#define STC_MTTKRP_MINB 3
+#endif
+
+#ifndef STC_MTTKRP_STAGE
+#define STC_MTTKRP_STAGE 40960
+#endif
+  static constexpr int kMinBlocks = STC_MTTKRP_MINB;
   static constexpr int kStageUnroll = 1;     // (2 and 3 measured: no gain, more registers)
-  static constexpr int kStageBytes = 40960;  // 80-item windows (3 CTAs x 58 KB; 96-item windows: +15 % time)
+  static constexpr int kStageBytes = STC_MTTKRP_STAGE;  // 80-item windows (3 CTAs x 58 KB; 96-item windows: +15 % time)
   struct __align__(16) Item {
     unsigned offb, offc;
     float v;
@@ -124,8 +134,7 @@ struct MttkrpOp {
     Frag<VEC> b, c;
   };
   struct State {
-    Frag<VEC> b, f;  // the open fiber's B[j,:] and its running sum_k T C[k,:]
-    bool open;
+    Frag<VEC> b;  // the current fiber's B[j,:]
   };
   STC_DEVICE Item load(long long p, bool first) const {
     const int j = ld_stream(jc + p);
@@ -143,35 +152,23 @@ struct MttkrpOp {
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
     STC_CHECK(!it.flag || (unsigned long long)(it.offb + lane_off) + VEC <= limitb, "MTTKRP gather outside B");
     STC_CHECK((unsigned long long)(it.offc + lane_off) + VEC <= limitc, "MTTKRP gather outside C");
+#ifdef STC_DIAG_NOGATHER  // diagnostic builds only (tools/build_variant.sh): time without the gathers
+    pre.b.v[0] = pre.c.v[0] = __int_as_float(it.offb ^ it.offc);
+#else
     if (it.flag) pre.b.load_gather(B + (it.offb + lane_off));
     pre.c.load_gather(C + (it.offc + lane_off));
+#endif
   }
-  STC_DEVICE static void init(State& st) {
-    st.b.zero();
-    st.f.zero();
-    st.open = false;
-  }
+  STC_DEVICE static void init(State& st) { st.b.zero(); }
   STC_DEVICE void accumulate(Frag<VEC>& acc, State& st, const Pre& pre, const Item& it) const {
-    const bool close = it.flag && st.open;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      const float t = fmaf(st.b.v[e], st.f.v[e], acc.v[e]);
-      acc.v[e] = close ? t : acc.v[e];
-      st.f.v[e] = it.flag ? 0.f : st.f.v[e];
       st.b.v[e] = it.flag ? pre.b.v[e] : st.b.v[e];
-      st.f.v[e] = fmaf(it.v, pre.c.v[e], st.f.v[e]);
-    }
-    st.open = true;
-  }
-  // close the open fiber into `acc` before `acc` is written out
-  STC_DEVICE static void finish(Frag<VEC>& acc, State& st) {
-    if (st.open) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(st.b.v[e], st.f.v[e], acc.v[e]);
-      st.f.zero();
-      st.open = false;
+      acc.v[e] = fmaf(it.v * st.b.v[e], pre.c.v[e], acc.v[e]);
     }
   }
+  STC_DEVICE static void finish(Frag<VEC>&, State&) {}
+
 };
 
 // 64-bit gathers for dense operands of 2^32 elements or more (e.g. 40 M-node
@@ -345,184 +342,15 @@ __host__ __device__ constexpr size_t merge_smem_bytes() {
          + (size_t)NG * merge_rend_stride<SUBW, Op>() * sizeof(int);                // staged row-end window
 }
 
-// One sub-warp ("group") per `ipg` merge items. The group stages a window of
-// its entries' items and of its rows' end offsets in shared memory (coalesced,
-// one round trip per window), then streams the gathers through a U-deep
-// register ring: the gather for entry q+U is issued while entry q is
-// accumulated, independent of row boundaries, so U loads stay in flight
-// across rows.
-template <int SUBW, int VEC, int EPI, bool ADD, int U, bool FULL, class Op>
-__global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, MergeShape ms, Op op) {
-  static_assert(U <= kStagePad, "ring deeper than the staging pad");
-  using Item = typename Op::Item;
+// CTA-level combine of the groups' head / tail partials (position order: tails of earlier
+// groups, then the head) and the cross-CTA carry fix-up by the last arriving CTA. Shared by
+// the staged and the register-pipelined merge kernels; called after a __syncthreads().
+template <int SUBW, int VEC, int EPI, bool ADD>
+STC_DEVICE void merge_combine(const SegOut& o, const MergeShape& ms, int sub, int lane, bool col_ok, int col0,
+                              long long zslab, float* Hs, float* Ts, int* Hrow, int* Trow) {
   constexpr int NG = 256 / SUBW;
   constexpr int SW = SUBW * VEC;
-  constexpr int CAP = merge_stage_cap<SUBW, Op>();
-  constexpr int CAPR = merge_rows_cap<SUBW, Op>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* Hs = reinterpret_cast<float*>(smem_raw);                       // [NG][SW]
-  float* Ts = Hs + NG * SW;                                             // [NG][SW]
-  int* Hrow = reinterpret_cast<int*>(Ts + NG * SW);                     // [NG]
-  int* Trow = Hrow + NG;                                                // [NG]
-  Item* items_all = reinterpret_cast<Item*>(Trow + NG);                 // [NG][CAP]
-  constexpr int IST = merge_item_stride<SUBW, Op>();
-  constexpr int RST = merge_rend_stride<SUBW, Op>();
-  int* rend_all = reinterpret_cast<int*>(items_all + NG * IST);         // [NG][RST]
-
-  const int sub = threadIdx.x / SUBW;
-  const int lane = threadIdx.x % SUBW;
-  const unsigned mask = subwarp_mask<SUBW>();
   const int cta = blockIdx.x;
-  const int slab = blockIdx.y;
-  const int z = blockIdx.z;
-  const int col0 = slab * SW + lane * VEC;
-  const bool col_ok = FULL || col0 < o.k;
-  Item* items = items_all + sub * IST;
-  int* rend = rend_all + sub * RST;
-
-  if (z) {
-    op.val += z * ms.batch_val_stride;
-    op.B += z * ms.batch_b_stride;
-    o.C += z * ms.batch_c_stride;
-    if constexpr (ADD) o.D += z * ms.batch_c_stride;
-  }
-  const long long zslab = ((long long)z * gridDim.y + slab) * ms.n_cta;
-  op.shift(col0);
-
-  const int g = min(cta * NG + sub, ms.n_groups);
-  const int2 s = ms.starts[g];
-  const int2 e = ms.starts[min(g + 1, ms.n_groups)];
-  const int row0 = s.x;
-  const int n_rows = e.x - s.x;   // rows whose end item this group owns
-  const int n_nnz = e.y - s.y;    // entries this group accumulates
-  STC_CHECK(n_rows >= 0 && n_nnz >= 0 && e.x <= o.m && n_nnz <= ms.ipg && n_rows <= ms.ipg,
-            "merge partition: group range");
-#ifdef STC_DBG_TIMING
-  const unsigned long long t_start = dbg_timer();
-#endif
-
-  // row ends of rows [row0 + rb, row0 + rb + CAPR), relative to s.y
-  int rb = 0;
-  auto stage_rows = [&](int base) {
-    __syncwarp(mask);
-    for (int t = lane; t < CAPR && base + t < n_rows; t += SUBW) {
-      rend[t] = ld_stream(o.rowptr + row0 + base + 1 + t) - s.y;
-      STC_CHECK(rend[t] >= 0 && rend[t] <= n_nnz, "row end outside the group's entries");
-    }
-    __syncwarp(mask);
-  };
-  stage_rows(0);
-  int first_start = 0;
-  if (lane == 0) {
-    first_start = (row0 < o.m) ? o.rowptr[row0] : s.y;
-    Hrow[sub] = -1;
-    Trow[sub] = -1;
-  }
-  first_start = __shfl_sync(mask, first_start, 0, SUBW);
-  const bool head_mid = (row0 < o.m) && (s.y > first_start);
-
-  int r = 0;                                        // current row = row0 + r
-  int cur_end = n_rows > 0 ? rend[0] : INT_MAX;      // relative end of the current row
-  int cur_start = first_start - s.y;                 // relative start (may be negative)
-  Frag<VEC> acc;
-  acc.zero();
-  typename Op::State fst;
-  Op::init(fst);
-
-  auto flush = [&]() {
-    Op::finish(acc, fst);
-    const int row = row0 + r;
-    if (r == 0 && head_mid) {
-      if (col_ok) acc.store_plain(&Hs[sub * SW + lane * VEC]);
-      if (lane == 0) Hrow[sub] = row;
-    } else if (col_ok) {
-      write_row<VEC, EPI, ADD>(o, row, col0, acc);
-    }
-    acc.zero();
-    ++r;
-    cur_start = cur_end;
-    if (r - rb == CAPR) {
-      rb = r;
-      stage_rows(rb);
-    }
-    cur_end = r < n_rows ? rend[r - rb] : INT_MAX;
-  };
-
-  typename Op::Pre ring[U];
-  for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
-    const int wn = min(CAP, n_nnz - w0);
-    STC_CHECK(wn + kStagePad <= IST, "staging window overflows its stride");
-    __syncwarp(mask);
-    // SU loads per lane in flight before their SMEM stores (one latency per SU * SUBW items)
-    constexpr int SU = Op::kStageUnroll;
-    for (int t0 = 0; t0 < wn + kStagePad; t0 += SU * SUBW) {
-      Item tmp[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const int t = t0 + u * SUBW + lane;
-        tmp[u] = t < wn ? op.load(s.y + w0 + t, w0 + t == 0) : Op::dummy();
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const int t = t0 + u * SUBW + lane;
-        if (t < wn + kStagePad) items[t] = tmp[u];
-      }
-    }
-    __syncwarp(mask);
-    int end_w = cur_end - w0;  // current row's end, relative to the window
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (col_ok) op.fetch(items[u], ring[u]);
-    int q0 = 0;
-    // the item of the next fetch is read from shared memory one step ahead, so the
-    // gather's address does not wait on that LDS (the window's pad covers the overrun)
-    // (SpMM only: MTTKRP's 16-byte items would spill at its register budget)
-    Item nf = items[U];
-    for (; q0 + U <= wn; q0 += U) {  // full ring turns: no bounds predicates
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        while (q0 + u >= end_w) {
-          flush();
-          end_w = cur_end - w0;
-        }
-        if constexpr (Op::kHoistItem) {
-          const Item cur = nf;
-          nf = items[q0 + u + 1 + U];
-          op.accumulate(acc, fst, ring[u], items[q0 + u]);
-          if (col_ok) op.fetch(cur, ring[u]);
-        } else {
-          op.accumulate(acc, fst, ring[u], items[q0 + u]);
-          if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // remainder of the window
-      if (q0 + u < wn) {
-        while (q0 + u >= end_w) {
-          flush();
-          end_w = cur_end - w0;
-        }
-        op.accumulate(acc, fst, ring[u], items[q0 + u]);
-      }
-    }
-  }
-  while (r < n_rows) flush();
-  Op::finish(acc, fst);
-  if (row0 + r < o.m && n_nnz > cur_start && r == n_rows) {
-    if (col_ok) acc.store_plain(&Ts[sub * SW + lane * VEC]);
-    if (lane == 0) Trow[sub] = row0 + r;
-  }
-#ifdef STC_DBG_TIMING
-  if (lane == 0 && g < (1 << 16) && blockIdx.y == 0 && blockIdx.z == 0) {
-    g_dbg[g][0] = t_start;
-    g_dbg[g][1] = dbg_timer();
-    g_dbg[g][2] = (unsigned long long)n_rows;
-    g_dbg[g][3] = ((unsigned long long)n_nnz << 32) | (unsigned)(threadIdx.x / 32 + (blockIdx.x << 8));
-  }
-#endif
-  __syncthreads();
-
   // ---- CTA-level combine (position order: tails of earlier groups, then head) ----
   __shared__ int head_row_s, tail_row_s;
   if (threadIdx.x == 0) head_row_s = tail_row_s = -1;
@@ -637,6 +465,190 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
     }
     __syncthreads();
   }
+}
+
+// One sub-warp ("group") per `ipg` merge items. The group stages a window of
+// its entries' items and of its rows' end offsets in shared memory (coalesced,
+// one round trip per window), then streams the gathers through a U-deep
+// register ring: the gather for entry q+U is issued while entry q is
+// accumulated, independent of row boundaries, so U loads stay in flight
+// across rows.
+template <int SUBW, int VEC, int EPI, bool ADD, int U, bool FULL, class Op>
+__global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, MergeShape ms, Op op) {
+  static_assert(U <= kStagePad, "ring deeper than the staging pad");
+  using Item = typename Op::Item;
+  constexpr int NG = 256 / SUBW;
+  constexpr int SW = SUBW * VEC;
+  constexpr int CAP = merge_stage_cap<SUBW, Op>();
+  constexpr int CAPR = merge_rows_cap<SUBW, Op>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* Hs = reinterpret_cast<float*>(smem_raw);                       // [NG][SW]
+  float* Ts = Hs + NG * SW;                                             // [NG][SW]
+  int* Hrow = reinterpret_cast<int*>(Ts + NG * SW);                     // [NG]
+  int* Trow = Hrow + NG;                                                // [NG]
+  Item* items_all = reinterpret_cast<Item*>(Trow + NG);                 // [NG][CAP]
+  constexpr int IST = merge_item_stride<SUBW, Op>();
+  constexpr int RST = merge_rend_stride<SUBW, Op>();
+  int* rend_all = reinterpret_cast<int*>(items_all + NG * IST);         // [NG][RST]
+
+  const int sub = threadIdx.x / SUBW;
+  const int lane = threadIdx.x % SUBW;
+  const unsigned mask = subwarp_mask<SUBW>();
+  const int cta = blockIdx.x;
+  const int slab = blockIdx.y;
+  const int z = blockIdx.z;
+  const int col0 = slab * SW + lane * VEC;
+  const bool col_ok = FULL || col0 < o.k;
+  Item* items = items_all + sub * IST;
+  int* rend = rend_all + sub * RST;
+
+  if (z) {
+    op.val += z * ms.batch_val_stride;
+    op.B += z * ms.batch_b_stride;
+    o.C += z * ms.batch_c_stride;
+    if constexpr (ADD) o.D += z * ms.batch_c_stride;
+  }
+  const long long zslab = ((long long)z * gridDim.y + slab) * ms.n_cta;
+  op.shift(col0);
+
+  const int g = min(cta * NG + sub, ms.n_groups);
+  const int2 s = ms.starts[g];
+  const int2 e = ms.starts[min(g + 1, ms.n_groups)];
+  const int row0 = s.x;
+  const int n_rows = e.x - s.x;   // rows whose end item this group owns
+  const int n_nnz = e.y - s.y;    // entries this group accumulates
+  STC_CHECK(n_rows >= 0 && n_nnz >= 0 && e.x <= o.m && n_nnz <= ms.ipg && n_rows <= ms.ipg,
+            "merge partition: group range");
+#ifdef STC_DBG_TIMING
+  const unsigned long long t_start = dbg_timer();
+#endif
+
+  // row ends of rows [row0 + rb, row0 + rb + CAPR), relative to s.y
+  int rb = 0;
+  auto stage_rows = [&](int base) {
+    __syncwarp(mask);
+    for (int t = lane; t < CAPR && base + t < n_rows; t += SUBW) {
+      rend[t] = ld_stream(o.rowptr + row0 + base + 1 + t) - s.y;
+      STC_CHECK(rend[t] >= 0 && rend[t] <= n_nnz, "row end outside the group's entries");
+    }
+    __syncwarp(mask);
+  };
+  stage_rows(0);
+  int first_start = 0;
+  if (lane == 0) {
+    first_start = (row0 < o.m) ? o.rowptr[row0] : s.y;
+    Hrow[sub] = -1;
+    Trow[sub] = -1;
+  }
+  first_start = __shfl_sync(mask, first_start, 0, SUBW);
+  const bool head_mid = (row0 < o.m) && (s.y > first_start);
+
+  int r = 0;                                        // current row = row0 + r
+  int cur_end = n_rows > 0 ? rend[0] : INT_MAX;      // relative end of the current row
+  int cur_start = first_start - s.y;                 // relative start (may be negative)
+  Frag<VEC> acc;
+  acc.zero();
+  typename Op::State fst;
+  Op::init(fst);
+
+  auto flush = [&]() {
+    Op::finish(acc, fst);
+    const int row = row0 + r;
+    if (r == 0 && head_mid) {
+      if (col_ok) acc.store_plain(&Hs[sub * SW + lane * VEC]);
+      if (lane == 0) Hrow[sub] = row;
+    } else if (col_ok) {
+      write_row<VEC, EPI, ADD>(o, row, col0, acc);
+    }
+    acc.zero();
+    ++r;
+    cur_start = cur_end;
+    if (r - rb == CAPR) {
+      rb = r;
+      stage_rows(rb);
+    }
+    cur_end = r < n_rows ? rend[r - rb] : INT_MAX;
+  };
+
+  typename Op::Pre ring[U];
+  for (int w0 = 0; w0 < n_nnz; w0 += CAP) {
+    const int wn = min(CAP, n_nnz - w0);
+    STC_CHECK(wn + kStagePad <= IST, "staging window overflows its stride");
+    __syncwarp(mask);
+    // SU loads per lane in flight before their SMEM stores (one latency per SU * SUBW items)
+    constexpr int SU = Op::kStageUnroll;
+#ifdef STC_DIAG_STAGE_ONCE  // diagnostic builds only: stage the first window and reuse it (wrong sums)
+    if (w0 == 0)
+#endif
+    for (int t0 = 0; t0 < wn + kStagePad; t0 += SU * SUBW) {
+      Item tmp[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int t = t0 + u * SUBW + lane;
+        tmp[u] = t < wn ? op.load(s.y + w0 + t, w0 + t == 0) : Op::dummy();
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int t = t0 + u * SUBW + lane;
+        if (t < wn + kStagePad) items[t] = tmp[u];
+      }
+    }
+    __syncwarp(mask);
+    int end_w = cur_end - w0;  // current row's end, relative to the window
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (col_ok) op.fetch(items[u], ring[u]);
+    int q0 = 0;
+    // the item of the next fetch is read from shared memory one step ahead, so the
+    // gather's address does not wait on that LDS (the window's pad covers the overrun)
+    // (SpMM only: MTTKRP's 16-byte items would spill at its register budget)
+    Item nf = items[U];
+    for (; q0 + U <= wn; q0 += U) {  // full ring turns: no bounds predicates
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        while (q0 + u >= end_w) {
+          flush();
+          end_w = cur_end - w0;
+        }
+        if constexpr (Op::kHoistItem) {
+          const Item cur = nf;
+          nf = items[q0 + u + 1 + U];
+          op.accumulate(acc, fst, ring[u], items[q0 + u]);
+          if (col_ok) op.fetch(cur, ring[u]);
+        } else {
+          op.accumulate(acc, fst, ring[u], items[q0 + u]);
+          if (col_ok) op.fetch(items[q0 + u + U], ring[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // remainder of the window
+      if (q0 + u < wn) {
+        while (q0 + u >= end_w) {
+          flush();
+          end_w = cur_end - w0;
+        }
+        op.accumulate(acc, fst, ring[u], items[q0 + u]);
+      }
+    }
+  }
+  while (r < n_rows) flush();
+  Op::finish(acc, fst);
+  if (row0 + r < o.m && n_nnz > cur_start && r == n_rows) {
+    if (col_ok) acc.store_plain(&Ts[sub * SW + lane * VEC]);
+    if (lane == 0) Trow[sub] = row0 + r;
+  }
+#ifdef STC_DBG_TIMING
+  if (lane == 0 && g < (1 << 16) && blockIdx.y == 0 && blockIdx.z == 0) {
+    g_dbg[g][0] = t_start;
+    g_dbg[g][1] = dbg_timer();
+    g_dbg[g][2] = (unsigned long long)n_rows;
+    g_dbg[g][3] = ((unsigned long long)n_nnz << 32) | (unsigned)(threadIdx.x / 32 + (blockIdx.x << 8));
+  }
+#endif
+  __syncthreads();
+
+  merge_combine<SUBW, VEC, EPI, ADD>(o, ms, sub, lane, col_ok, col0, zslab, Hs, Ts, Hrow, Trow);
 }
 
 // ---------------------------------------------------------------------------

@@ -370,11 +370,11 @@ extern "C" int stc_coo_segments(long long nnz, const int* rows, int* seg_rows, i
 
 // ---- MTTKRP ------------------------------------------------------------------------
 
-extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
-                                   const float* vals, long long nnz, int n_j, const float* B, long long ldb,
-                                   int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
-                                   const int* partition, int items_per_group, void* ws, size_t ws_bytes,
-                                   void* stream) {
+namespace {
+int mttkrp_common(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd, const float* vals,
+                  long long nnz, int n_j, const float* B, long long ldb, int n_k, const float* C, long long ldcf,
+                  float* M, long long ldm, int variant, const int* partition, int items_per_group, void* ws,
+                  size_t ws_bytes, void* stream) {
   if (n_seg < 0 || rank < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
   if (nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "nnz exceeds int32 index range");
   if (n_seg == 0 || rank == 0) return STC_OK;
@@ -418,6 +418,17 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
   op.limitc = (unsigned long long)n_k * ldcf;
   return dispatch_subw<1, EPI_NONE, false>(subw, o, ms, op, L);
 }
+}  // namespace
+
+extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd, const int* kcrd,
+                                   const float* vals, long long nnz, int n_j, const float* B, long long ldb,
+                                   int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
+                                   const int* partition, int items_per_group, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  return mttkrp_common(n_seg, rank, seg_ptr, jcrd, kcrd, vals, nnz, n_j, B, ldb, n_k, C, ldcf, M, ldm, variant,
+                       partition, items_per_group, ws, ws_bytes, stream);
+}
+
 
 #ifdef STC_DBG_TIMING
 // Diagnostic build only: copy the per-group timing stamps of the last merge launch.

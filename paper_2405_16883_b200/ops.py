@@ -514,8 +514,9 @@ def sparse_attention(rowptr, colidx, Q, K, V, *, maskvals=None, scale: float | N
 def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tensor, *,
                 variant: str = "merge", partition: MergePartition | None = None,
                 workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """``M[s, :] = sum_{p in segment s} T[p] * B[j[p], :] * C[k[p], :]`` -> [n_seg, R]
-    (evaluated per (i,j) fiber: B[j, :] times the fiber's sum of T * C[k, :])."""
+    """``M[s, :] = sum_{p in segment s} T[p] * B[j[p], :] * C[k[p], :]`` -> [n_seg, R]: per entry
+    the term (T[p] * B[j]) * C[k] in entry order (the reference's term order), with B[j, :]
+    gathered once per (i, j) fiber."""
     require_cuda(jcrd, kcrd, vals, B, C)
     R = B.shape[1]
     if C.shape[1] != R or B.stride(1) != 1 or C.stride(1) != 1:

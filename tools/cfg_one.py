@@ -48,7 +48,8 @@ def cfg2():
     return lambda: ops.spmm_csr(R, C, V, Z, out=out, relu=True, variant="merge", partition=part, workspace=ws)
 
 
-fn = {"2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5}[sys.argv[1]]()
-for _ in range(3):
-    fn()
-torch.cuda.synchronize()
+if __name__ == "__main__":
+    fn = {"2": cfg2, "3": cfg3, "4": cfg4, "5": cfg5}[sys.argv[1]]()
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
