@@ -113,7 +113,13 @@ struct MttkrpOp {
   // reference's term order, engine.py:577-644) -- 3 ops per element. (The fiber-sum form
   // B[j,:] * sum_k T C[k,:] costs 5 ops per element with its open/close selects: cfg5
   // 135 -> 131 us; its loop alone 68 -> 53 us in a diagnostic build without gathers.)
-  static constexpr int kRing = VEC == 4 ? 4 : 8;
+#ifndef STC_MTTKRP_RING
+#define STC_MTTKRP_RING 4
+#endif
+#ifndef STC_MTTKRP_SU
+#define STC_MTTKRP_SU 2
+#endif
+  static constexpr int kRing = VEC == 4 ? STC_MTTKRP_RING : 8;
   static constexpr bool kHoistItem = false;
 #ifndef STC_MTTKRP_MINB
 #define STC_MTTKRP_MINB 3
@@ -123,7 +129,7 @@ struct MttkrpOp {
 #define STC_MTTKRP_STAGE 40960
 #endif
   static constexpr int kMinBlocks = STC_MTTKRP_MINB;
-  static constexpr int kStageUnroll = 1;     // (2 and 3 measured: no gain, more registers)
+  static constexpr int kStageUnroll = STC_MTTKRP_SU;  // item loads per lane in flight while staging (1: 130.6 us, 2: 129.1, 4: 129.0)
   static constexpr int kStageBytes = STC_MTTKRP_STAGE;  // 80-item windows (3 CTAs x 58 KB; 96-item windows: +15 % time)
   struct __align__(16) Item {
     unsigned offb, offc;
