@@ -198,6 +198,17 @@ int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd
                         const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                         void* stream);
 
+/* ---- device-side construction --------------------------
+ * Exact duplicate folding: out[s] = fsum(vals[starts[s] .. starts[s+1])), the correctly
+ * rounded float64 sum that Python's math.fsum returns (Shewchuk expansion + half-even
+ * correction), bit for bit; replaces the reference's per-coordinate fsum in
+ * build_from_entries (tensor.py:238-241). Where fsum raises, out[s] is a NaN with the
+ * payload below (-inf + inf: ValueError; intermediate overflow: OverflowError).         */
+#define STC_FSUM_INF_MINUS_INF 0x7ff8dead00000001LL
+#define STC_FSUM_OVERFLOW 0x7ff8dead00000002LL
+int stc_fsum_segments_f64(long long n_seg, const long long* starts, const double* vals, double* out,
+                          void* stream);
+
 /* ---- sparse x sparse on CSR operands ------------------
  * SpGEMM C(i,k) = A(i,j) * B(j,k), CSR x CSR -> CSR, replacing the reference's
  * workspace plan ([i,j,k], Workspace over k: engine.py:577-644, 71-90). Output

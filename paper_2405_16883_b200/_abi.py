@@ -37,6 +37,9 @@ VARIANTS = {"row": VARIANT_ROW, "merge": VARIANT_MERGE, "coltile": VARIANT_COLTI
 EPILOGUE_NONE = 0
 EPILOGUE_RELU = 1
 
+FSUM_INF_MINUS_INF = 0x7FF8DEAD00000001
+FSUM_OVERFLOW = 0x7FF8DEAD00000002
+
 EWISE_UNION = 0
 EWISE_INTERSECT = 1
 
@@ -74,6 +77,7 @@ SIGNATURES = {
                                             _ll, _p, _ll, _ll, _f, _p, _ll, _ll, _p, _sz, _p]),
     "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _i, _p, _i,
                                  _p, _sz, _p]),
+    "stc_fsum_segments_f64": (_i, [_ll, _p, _p, _p, _p]),
     "stc_spgemm_products_temp_bytes": (_sz, [_i]),
     "stc_spgemm_products": (_i, [_i, _p, _p, _p, _p, _p, _sz, _p]),
     "stc_spgemm_workspace_bytes": (_sz, [_i, _i, _ll]),

@@ -138,11 +138,6 @@ __host__ __device__ inline int dense_words(int p) { return (p + 31) / 32; }
 __host__ __device__ inline size_t dense_warp_bytes(int p) {
   return (size_t)dense_words(p) * 4 + (size_t)((p + 31) / 32 * 32) * 4;
 }
-inline int dense_warps_per_cta(int p) {
-  const size_t per = dense_warp_bytes(p);
-  int w = (int)((200u * 1024u) / per);
-  return w > 8 ? 8 : w;
-}
 
 __global__ void spgemm_dense_kernel(int phase, int m, int p, const int* __restrict__ ap, const int* __restrict__ aj,
                                     const float* __restrict__ av, const int* __restrict__ bp,

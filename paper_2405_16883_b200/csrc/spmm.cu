@@ -194,6 +194,7 @@ extern "C" int stc_merge_plan_items_per_group(int m, long long nnz, int k, int b
 
 extern "C" long long stc_coltile_plan_ints(int m, int n, long long nnz) {
   if (m < 0 || n < 0 || nnz < 0) return -1;
+  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_CHUNK) * CTT_ROWS + 1 >= INT32_MAX) return -1;
   const CttLayout lay = ctt_layout(m, n, nnz);
   if (lay.max_entries >= INT32_MAX) return -1;
   return lay.total_ints;
@@ -203,6 +204,8 @@ extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, 
                                 const float* vals, int* plan, long long plan_ints, void* stream) {
   if (m < 0 || n < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
   if (!plan || !rowptr || (nnz && (!colidx || !vals))) return fail(STC_EINVAL, "null pointer");
+  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_CHUNK) * CTT_ROWS + 1 >= INT32_MAX)
+    return fail(STC_EUNSUPPORTED, "COLTILE plan: m * ceil(n / 64) slots exceed int32");
   const CttLayout lay = ctt_layout(m, n, nnz);
   if (lay.max_entries >= INT32_MAX) return fail(STC_EUNSUPPORTED, "COLTILE plan exceeds int32 entries");
   if (plan_ints < lay.total_ints)

@@ -437,7 +437,7 @@ def _spmm_rows(ctx: _Ctx, m: _SpmmTerm, addend: torch.Tensor | None = None, relu
     K = Bd.shape[1]
     key = (row_dim,)
     stats = _stats(A, view, key)
-    variant = ctx.variant or ops.choose_variant(stats, K, aligned=(K % 4 == 0))
+    variant = ctx.variant or ops.choose_variant(stats, K, aligned=(K % 4 == 0), n_cols=Bd.shape[0])
     if variant not in ("row", "merge", "coltile"):
         raise ValueError(f"unknown variant {variant!r}")
     partition = None

@@ -68,15 +68,33 @@ def row_stats(rowptr: torch.Tensor) -> RowStats:
     return RowStats(m, int(nnz), int(mx))
 
 
-def choose_variant(stats: RowStats, k: int, aligned: bool = True) -> str:
+def choose_variant(stats: RowStats, k: int, aligned: bool = True, n_cols: int | None = None) -> str:
     """The reference's plan for C(i,k)=A(i,j)*B(j,k) is always [i,j,k] with
     tiles {k} (scheduler.py / tiling.py); on the device the same plan splits
-    into three variants by the shape of the data."""
-    if k >= COLTILE_MIN_K and aligned:
+    into three variants by the shape of the data.
+
+    COLTILE reads every B row of a column slab once per 128-row block, i.e. B's bytes
+    m / 128 times, where the gather variants read nnz rows: it is chosen only for wide
+    dense operands when A is dense enough (nnz >= m * n / 128) and its plan fits int32."""
+    if k >= COLTILE_MIN_K and aligned and coltile_fits(stats, n_cols):
         return "coltile"
     if stats.skew > MERGE_SKEW_THRESHOLD or stats.max_row > 4096:
         return "merge"
     return "row"
+
+
+def coltile_fits(stats: RowStats, n_cols: int | None) -> bool:
+    """COLTILE pays off (and its plan is addressable) for this matrix: density at least
+    1/128 and m * ceil(n / 64) plan slots below 2^31. Without ``n_cols`` (unknown width)
+    only the density against the widest possible square operand is not checked."""
+    if n_cols is None:
+        return True
+    m = stats.m
+    if m == 0 or n_cols == 0:
+        return False
+    if m * (-(-n_cols // 64)) >= 2**31 - 1:
+        return False
+    return stats.nnz * 128 >= m * n_cols
 
 
 @dataclass
@@ -239,7 +257,7 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
         raise ValueError("addend must be an (m, k) row-major tensor")
     if variant is None:
         stats = stats or row_stats(rowptr)
-        variant = choose_variant(stats, k, aligned=(k % 4 == 0))
+        variant = choose_variant(stats, k, aligned=(k % 4 == 0), n_cols=n)
     v = _abi.VARIANTS[variant]
     ipg = 0
     plan_ptr = None

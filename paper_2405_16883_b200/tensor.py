@@ -320,7 +320,7 @@ def _assemble(shape, fmt: TensorFormat, coords: torch.Tensor, vals: torch.Tensor
     order = fmt.order
     coords = coords.to(torch.long).reshape(n, order)
     perm_cols = coords[:, list(fmt.mode_ordering)] if order else coords
-    if n:
+    if n and order:
         extents = [fmt.level_extent(k) for k in range(order)]
         perm = _lexsort_rows([perm_cols[:, k] for k in range(order)], extents)
         perm_cols = perm_cols[perm]
@@ -336,29 +336,26 @@ def _assemble(shape, fmt: TensorFormat, coords: torch.Tensor, vals: torch.Tensor
 def build_from_entries(shape, fmt: TensorFormat, entries, name: str = "T", device=None) -> Tensor:
     """Tensor from (coordinate tuple, value) pairs.
 
-    Duplicates are summed exactly (``math.fsum``), explicit zeros are kept, and
-    the coordinate checks raise the reference's exceptions (`tensor.py:222-242`).
-    Values are rounded to float32 once, after summation.
+    Duplicates are summed exactly (``math.fsum``; on a CUDA device by the bit-identical
+    ``stc_fsum_segments_f64``), explicit zeros are kept, and the coordinate checks raise
+    the reference's exceptions (`tensor.py:222-242`). Values are rounded to float32 once,
+    after summation.
     """
     shape = tuple(int(s) for s in shape)
     if fmt.shape != shape:
         raise ShapeError(f"format shape {fmt.shape} != requested shape {shape}")
-    acc: dict[tuple, list[float]] = {}
+    coords, vals = [], []
     for coord, value in entries:
         coord = tuple(int(c) for c in coord)
         if len(coord) != len(shape):
             raise ShapeError(f"coordinate {coord} has wrong arity for shape {shape}")
         if any(c < 0 or c >= s for c, s in zip(coord, shape)):
             raise IndexError(f"coordinate {coord} out of bounds for shape {shape}")
-        acc.setdefault(coord, []).append(float(value))
-    keys = sorted(acc)
-    coords = np.asarray(keys, dtype=np.int64).reshape(len(keys), len(shape))
-    vals = np.asarray(
-        [acc[k][0] if len(acc[k]) == 1 else math.fsum(acc[k]) for k in keys], dtype=np.float64
-    )
-    dev = _as_device(device)
-    return _assemble(shape, fmt, torch.from_numpy(coords).to(dev),
-                     torch.from_numpy(vals).to(VALUE_DTYPE).to(dev), name)
+        coords.append(coord)
+        vals.append(float(value))
+    # duplicates summed exactly (fsum per coordinate): on the device when it is CUDA
+    return from_arrays(shape, fmt, np.asarray(coords, dtype=np.int64).reshape(len(coords), len(shape)),
+                       np.asarray(vals, dtype=np.float64), name, device, duplicates="sum")
 
 
 def from_arrays(shape, fmt: TensorFormat, coords, values, name: str = "T", device=None,
@@ -366,7 +363,7 @@ def from_arrays(shape, fmt: TensorFormat, coords, values, name: str = "T", devic
     """Vectorised construction from an (n, order) coordinate array and n values.
 
     ``duplicates="sum"`` folds repeated coordinates like ``build_from_entries``
-    (exact ``fsum`` on the host for the repeated groups); ``"error"`` rejects
+    (exact fsum per coordinate, on the device for CUDA storage); ``"error"`` rejects
     them; ``"unique"`` trusts the caller. Runs on ``device`` (default CUDA).
     """
     shape = tuple(int(s) for s in shape)
@@ -382,26 +379,52 @@ def from_arrays(shape, fmt: TensorFormat, coords, values, name: str = "T", devic
         hi = c.max(0).values
         if bool((lo < 0).any()) or any(int(hi[d]) >= shape[d] for d in range(len(shape))):
             raise IndexError(f"coordinates out of bounds for shape {shape}")
-    if duplicates != "unique" and n > 1:
+    if duplicates != "unique" and n > 1 and not shape:  # order 0: every entry is the same coordinate
+        if duplicates == "error":
+            raise ValueError("duplicate coordinates")
+        c, v = _fold_duplicates(c[:1].expand(n, 0).to(dev), v.to(torch.float64).to(dev),
+                                torch.ones(n - 1, dtype=torch.bool, device=dev))
+    elif duplicates != "unique" and n > 1:
         perm = _lexsort_rows([c[:, d] for d in range(len(shape))], list(shape))
         cs = c[perm]
         same = (cs[1:] == cs[:-1]).all(1)
         if bool(same.any()):
             if duplicates == "error":
                 raise ValueError("duplicate coordinates")
-            # exact host-side fsum per repeated group, like build_from_entries
-            cs_np = cs.cpu().numpy()
-            v_np = v.to(torch.float64)[perm.to(v.device)].cpu().numpy()
-            first = np.ones(n, dtype=bool)
-            first[1:] = ~same.cpu().numpy()
-            starts = np.flatnonzero(first)
-            ends = np.append(starts[1:], n)
-            out = v_np[starts].copy()
-            for g in np.flatnonzero(ends - starts > 1):
-                out[g] = math.fsum(v_np[starts[g]:ends[g]])
-            c = torch.from_numpy(cs_np[starts])
-            v = torch.from_numpy(out)
+            c, v = _fold_duplicates(cs, v.to(torch.float64)[perm.to(v.device)], same)
     return _assemble(shape, fmt, c.to(dev), v.to(dev).to(VALUE_DTYPE), name)
+
+
+def _fold_duplicates(cs: torch.Tensor, vs: torch.Tensor, same: torch.Tensor):
+    """Sum the values of equal (sorted, adjacent) coordinates exactly, like the reference's
+    ``math.fsum`` per coordinate (`tensor.py:238-241`): one float64 result per distinct
+    coordinate, correctly rounded. On a CUDA device the groups are summed by
+    ``stc_fsum_segments_f64`` (the same algorithm, bit for bit); host tensors use fsum."""
+    n = vs.numel()
+    first = torch.ones(n, dtype=torch.bool, device=cs.device)
+    first[1:] = ~same
+    starts = torch.nonzero(first).flatten()
+    if cs.is_cuda:
+        from . import _abi
+
+        vs = vs.to(cs.device).contiguous()
+        bounds = torch.cat([starts, torch.tensor([n], device=cs.device)]).to(torch.int64).contiguous()
+        out = torch.empty(starts.numel(), dtype=torch.float64, device=cs.device)
+        _abi.check(_abi.lib().stc_fsum_segments_f64(starts.numel(), bounds.data_ptr(), vs.data_ptr(), out.data_ptr(),
+                                                    _abi.stream_handle()), "stc_fsum_segments_f64")
+        bits = out.view(torch.int64)
+        if bool((bits == _abi.FSUM_INF_MINUS_INF).any()):
+            raise ValueError("-inf + inf in fsum")
+        if bool((bits == _abi.FSUM_OVERFLOW).any()):
+            raise OverflowError("intermediate overflow in fsum")
+        return cs[starts], out
+    v_np = vs.cpu().numpy()
+    st_np = starts.cpu().numpy()
+    ends = np.append(st_np[1:], n)
+    out = v_np[st_np].copy()
+    for g in np.flatnonzero(ends - st_np > 1):
+        out[g] = math.fsum(v_np[st_np[g]:ends[g]])
+    return cs[starts], torch.from_numpy(out)
 
 
 def csr_from_arrays(rowptr, colidx, values, shape, name: str = "A", device=None,

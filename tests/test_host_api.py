@@ -322,3 +322,19 @@ def test_storage_matches_reference_goldens():
     assert t.storage.levels[1].pos.tolist() == pos.tolist()
     assert t.storage.levels[1].crd.tolist() == crd.tolist()
 
+
+
+def test_oracle_module_alias():
+    """`from sparsetc.oracle import eval_dense` (reference __init__.py:27) has a counterpart."""
+    from paper_2405_16883_b200.oracle import eval_dense
+
+    assert eval_dense is st.eval_dense
+
+
+def test_build_from_entries_scalar_and_exact_duplicate_sum():
+    """Duplicates are summed exactly (fsum, reference tensor.py:238-241), scalars included."""
+    t = st.build_from_entries((), st.dense_format(()), [((), 1.5), ((), 2.25)], device="cpu")
+    assert float(st.to_dense(t)) == 3.75
+    t = st.build_from_entries((2, 3), st.csr(2, 3), [((0, 1), 1e16), ((0, 1), 1.0), ((0, 1), -1e16), ((1, 2), 5.0)],
+                              device="cpu")
+    assert st.to_dense(t)[0, 1] == 1.0 and st.nnz(t) == 2
