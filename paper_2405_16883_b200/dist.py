@@ -57,3 +57,74 @@ def allgather_rows(local: torch.Tensor, shards: list[tuple[int, int]]) -> torch.
     bufs = [torch.empty_like(padded) for _ in range(world)]
     dist.all_gather(bufs, padded)
     return torch.cat([b[: r1 - r0] for b, (r0, r1) in zip(bufs, shards)], dim=0)
+
+
+class ShardedCSR:
+    """This rank's row shard of a CSR matrix, on its own GPU, with a cached SpMM plan.
+
+    The rows are split into ``world`` contiguous ranges of equal rows + nnz work
+    (``nnz_balanced_row_shards``); the column space is not split, so the dense operand of an
+    SpMM is the full (replicated or all-gathered) matrix and every rank's output rows are its
+    own: no reduction across ranks. ``spmm_impl`` replaces the CUDA op (``ops.spmm_csr``)
+    only in host-side tests of the partition / exchange logic.
+    """
+
+    def __init__(self, rowptr, colidx, vals, shape, rank: int, world: int, device=None, spmm_impl=None):
+        self.shape = (int(shape[0]), int(shape[1]))
+        self.rank, self.world = rank, world
+        self.shards = nnz_balanced_row_shards(rowptr, world)
+        self.r0, self.r1 = self.shards[rank]
+        rp, ci, v = shard_csr(rowptr, colidx, vals, self.r0, self.r1)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.rowptr = torch.as_tensor(rp).to(dev, torch.int32)
+        self.colidx = torch.as_tensor(ci).to(dev, torch.int32)
+        self.vals = torch.as_tensor(v).to(dev, torch.float32)
+        self._impl = spmm_impl
+        self._plan = {}
+
+    @property
+    def local_rows(self) -> int:
+        return self.r1 - self.r0
+
+    def spmm(self, B: torch.Tensor, relu: bool = False) -> torch.Tensor:
+        """Rows [r0, r1) of act(A @ B) for the full dense operand B (n x k)."""
+        if B.shape[0] != self.shape[1]:
+            raise ValueError(f"dense operand has {B.shape[0]} rows, matrix has {self.shape[1]} columns")
+        if self._impl is not None:
+            return self._impl(self.rowptr, self.colidx, self.vals, B, relu)
+        from . import ops
+
+        k = B.shape[1]
+        if k not in self._plan:
+            stats = ops.row_stats(self.rowptr)
+            variant = ops.choose_variant(stats, k, aligned=k % 4 == 0, n_cols=self.shape[1])
+            part = ops.merge_partition(self.rowptr, self.vals.numel(), k=k, colidx=self.colidx, vals=self.vals,
+                                       max_row=stats.max_row) if variant == "merge" else None
+            self._plan[k] = (stats, variant, part)
+        stats, variant, part = self._plan[k]
+        return ops.spmm_csr(self.rowptr, self.colidx, self.vals, B, relu=relu, variant=variant, partition=part,
+                            stats=stats)
+
+
+def gcn_forward_sharded(A: ShardedCSR, X_local: torch.Tensor, W1: torch.Tensor, W2: torch.Tensor) -> torch.Tensor:
+    """Two-layer GCN forward on a row-sharded graph (configs[1] split over the ranks):
+    ``Z1 = X W1`` on local rows -> all-gather Z1 -> ``H = ReLU(A Z1)`` (local rows) ->
+    ``Z2 = H W2`` -> all-gather Z2 -> ``O = A Z2`` (local rows). The exchanges move the
+    layers' GEMM outputs (n x 128 fp32, NCCL all-gather over NVLink on GPUs) -- the one real
+    exchange step of the path; the SpMMs run the CUDA kernels on each rank's shard.
+    Returns this rank's rows of O."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        Z1 = _gather(X_local @ W1, A.shards)
+        H = A.spmm(Z1, relu=True)
+        Z2 = _gather(H @ W2, A.shards)
+        return A.spmm(Z2)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def _gather(local: torch.Tensor, shards) -> torch.Tensor:
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return local
+    return allgather_rows(local, shards)

@@ -1,6 +1,7 @@
 """N>1 host logic on CPU with gloo (world_size 2): nnz-balanced row sharding,
 row-disjoint partial SpMMs reassembled by all-gather, and the max-over-ranks
-timing reduction used by bench.py."""
+timing reduction used by bench.py (the product's sharded GCN path:
+tests/test_distributed_product.py)."""
 
 import os
 import socket
@@ -22,20 +23,26 @@ def _free_port():
     return p
 
 
+def _csr_matmul(rp, ci, v, X):
+    """Local row-shard product on the host (float64 torch CSR): the CUDA kernels need a GPU;
+    this test covers the sharding, exchange and reduction logic."""
+    A = torch.sparse_csr_tensor(torch.as_tensor(rp).long(), torch.as_tensor(ci).long(),
+                                torch.as_tensor(v).double(), size=(len(rp) - 1, X.shape[0]))
+    return A @ torch.as_tensor(X).double()
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from oracle import native
-
         A, X, _, _ = synthetic.cfg2(n=3000, feat=16)
         shards = sdist.nnz_balanced_row_shards(A.rowptr, world)
         r0, r1 = shards[rank]
         rp, ci, v = sdist.shard_csr(A.rowptr, A.colidx, A.vals, r0, r1)
-        local = torch.from_numpy(native.spmm_csr(rp, ci, v, X))
+        local = _csr_matmul(rp, ci, v, X)
         full = sdist.allgather_rows(local, shards)
-        want = native.spmm_csr(A.rowptr, A.colidx, A.vals, X)
-        ok = bool(np.array_equal(full.numpy(), want))
+        want = _csr_matmul(A.rowptr, A.colidx, A.vals, X)
+        ok = bool(torch.equal(full, want))
         t = sdist.max_over_ranks(float(rank + 1))
         q.put((rank, ok, t, shards))
     finally:
