@@ -29,9 +29,10 @@ operand), so the iteration space is exactly the reference's:
 
 Operands stored in an order that violates the loop order are converted first
 (`engine.py:313-318`). Tiling is bit-neutral in the reference
-(`tests/test_acceptance.py:85-98`) and does not change the walk. OpCounter fields
-on this path are work estimates (rows produced per loop, products, sums), not the
-interpreter's exact counts.
+(`tests/test_acceptance.py:85-98`) and does not change the walk. The OpCounter of this
+path is the interpreter's exact count, from a second breadth-first enumeration of the
+reference's own loop nest (tile blocks, intersection order, vectorised tails and all:
+``walk_count.count_ops``), pinned to the reference's counters on every fixture.
 """
 
 from __future__ import annotations
@@ -96,6 +97,32 @@ class _Cursor:
             self.lo, self.hi = self.lo[rows], self.hi[rows]
         else:
             self.p = self.p[rows]
+
+    def clone(self) -> "_Cursor":
+        c = object.__new__(_Cursor)
+        c.__dict__.update(self.__dict__)
+        return c
+
+    @staticmethod
+    def cat(parts: list) -> "_Cursor":
+        """Row-wise concatenation of clones of one cursor (same depth)."""
+        c = parts[0].clone()
+        if c.coo:
+            c.lo = torch.cat([x.lo for x in parts])
+            c.hi = torch.cat([x.hi for x in parts])
+        else:
+            c.p = torch.cat([x.p for x in parts])
+        return c
+
+    def seg_len(self) -> torch.Tensor:
+        """Per row, the number of coordinates the next (sparse) level iterates: the segment
+        length of a compressed level, the distinct values of the bound run of a coordinate level
+        (the reference's ``segment_coords``, engine.py:111-114, 150-152)."""
+        if self.coo:
+            rows, _ = self.clone().expand()
+            return torch.bincount(rows, minlength=self.lo.numel())
+        pos = self.t.storage.levels[self.depth].pos.to(torch.long)
+        return pos[self.p + 1] - pos[self.p]
 
     # -- sorted search keys per level (parent id * extent + coordinate) --------------
     def _level_key(self, d: int) -> torch.Tensor:
@@ -192,7 +219,7 @@ def _dense_strides(t: Tensor) -> list:
     return strides
 
 
-def _walk_term(term, tensor_of, loop_order, out_chain, ext, dev, counter):
+def _walk_term(term, tensor_of, loop_order, out_chain, ext, dev):
     """Returns (visited keys as linear out-chain offsets (unique, sorted), key of each
     final row, product of each final row) for one product term."""
     term_vars = {v for a in term for v in a.indices}
@@ -264,7 +291,6 @@ def _walk_term(term, tensor_of, loop_order, out_chain, ext, dev, counter):
         n_rows = int(coord.numel())
         if n_rows > MAX_ROWS:
             raise TooLargeForGenericWalk(f"loop nest frontier of {n_rows} rows")
-        counter.add(0, 0, n_rows)
         if si == last_out:
             keys = torch.unique(lin_of(coords))
     # product of every factor at each full binding (float64)
@@ -277,7 +303,6 @@ def _walk_term(term, tensor_of, loop_order, out_chain, ext, dev, counter):
         for d, u in enumerate(a.indices):
             off += coords[u] * strides[d]
         prod = prod * t.storage.values.to(torch.float64)[off]
-    counter.add(max(len(term) - 1, 0) * n_rows, n_rows, 0)
     row_key = lin_of(coords) if out_chain else torch.zeros(n_rows, dtype=torch.long, device=dev)
     return keys, row_key, prod
 
@@ -304,9 +329,13 @@ def execute_generic(sched: Schedule, tensor_of: dict, out_fmt: TensorFormat, cou
     out_vars = e.output_indices
     out_chain = tuple(out_vars[d] for d in out_fmt.mode_ordering)
     shape = tuple(ext[v] for v in out_vars)
+    # the reference interpreter's exact counters: its loop nest enumerated on the device
+    from .walk_count import count_ops
+
+    counter.add(*count_ops(sched, walk_of, out_fmt))
     all_keys, all_rows, all_prod = [], [], []
     for term in e.terms():
-        keys, row_key, prod = _walk_term(term, walk_of, order, out_chain, ext, dev, counter)
+        keys, row_key, prod = _walk_term(term, walk_of, order, out_chain, ext, dev)
         all_keys.append(keys)
         all_rows.append(row_key)
         all_prod.append(prod)

@@ -33,9 +33,13 @@ def random_tensor(rng, shape, fmt_name, density, name, integer=False, device=Non
     return st.build_from_entries(shape, fmt, entries, name=name, device=device)
 
 
-def random_expression(rng, extent_cap=8, densities=(0.1, 0.5, 1.0), integer=False, device=None):
+def random_expression(rng, extent_cap=8, densities=(0.1, 0.5, 1.0), integer=False, device=None, big=None):
+    """The reference's random-expression strategy; ``big`` (optional) gives one index an extent
+    in [65, big], so tiled loops run several 64-wide blocks."""
     pool = [st.IndexVar(n) for n in ("i", "j", "k")[: rng.integers(1, 4)]]
     ext = {v: int(rng.integers(1, extent_cap + 1)) for v in pool}
+    if big:
+        ext[pool[int(rng.integers(len(pool)))]] = int(rng.integers(65, big + 1))
     terms = []
     used = set()
     counter = 0
