@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define STC_ABI_VERSION 1
+#define STC_ABI_VERSION 2  /* 2: L2-persisting entry points removed, stc_fsum_segments_f64 added */
 
 #define STC_OK 0
 #define STC_EINVAL (-1)       /* null / misaligned pointer, bad shape        */

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_only_entry_points():
     lib = _abi.load_library()
-    assert lib.stc_abi_version() == 1
+    assert lib.stc_abi_version() == 2
     assert lib.stc_last_error() == b""
     assert lib.stc_merge_path_groups(10, 30, 8) == 7   # 2 items per row end + 1 per entry: ceil(50 / 8)
     assert lib.stc_merge_path_groups(0, 0, 8) == 0
@@ -111,3 +111,10 @@ def test_sparse_sparse_ops_fail_loudly_without_cuda():
     for src in ("C(i,k) = A(i,j) * B(j,k)", "C(i,j) = A(i,j) + B(i,j)", "C(i,j) = A(i,j) * B(i,j)"):
         with pytest.raises(_abi.ExtensionUnavailable):
             st.run(st.parse(src, {"A": A, "B": B}))
+
+
+def test_fsum_entry_point_validation_without_gpu():
+    lib = _abi.load_library()
+    assert lib.stc_fsum_segments_f64(-1, None, None, None, None) == _abi.STC_EINVAL
+    assert lib.stc_fsum_segments_f64(0, None, None, None, None) == _abi.STC_OK
+    assert lib.stc_fsum_segments_f64(3, None, None, None, None) == _abi.STC_EINVAL
