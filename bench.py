@@ -597,7 +597,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if not args.no_e2e:
-        e_ms, h2d, d2h, O_host = work.e2e(steps=max(3, min(args.steps, 20)), warmup=3)
+        e_ms, h2d, d2h, O_host = work.e2e(steps=max(3, min(args.steps, 50)), warmup=3)
         if world > 1:
             t = torch.tensor([e_ms], device=device, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
