@@ -47,3 +47,11 @@ print("corr(end, fibers) %.2f  (fibers per group p10/p50/p90 %d/%d/%d)" % (
     np.corrcoef(end, fib[:len(end)])[0, 1], *np.percentile(fib, [10, 50, 90])))
 gathers = nnz + fib[:len(end)]
 print("corr(end, entries + fibers) %.2f" % np.corrcoef(end, gathers)[0, 1])
+# least squares: finish = a + b * fibers + c * rows; what an equal-cost partition would give
+X = np.stack([np.ones(len(end)), fib[:len(end)].astype(float), rows.astype(float)], 1)
+coef, *_ = np.linalg.lstsq(X, end, rcond=None)
+pred = X @ coef
+print("fit a=%.1f us, per fiber %.4f us, per row %.4f us; residual sd %.2f us" % (
+    coef[0], coef[1], coef[2], np.std(end - pred)))
+print("equal-cost groups would finish near %.1f us (+ residual p99 %.1f)" % (
+    pred.mean(), np.percentile(end - pred, 99)))
