@@ -50,6 +50,35 @@ def _as_device(device) -> torch.device:
     return default_device() if device is None else torch.device(device)
 
 
+class StorageArray(torch.Tensor):
+    """A storage buffer as the reference exposes it: read-only, numpy-convertible.
+
+    The reference freezes its level arrays (``arr.flags.writeable = False``,
+    `tensor.py:53-56, 71-72`), so ``t.storage.values[0] = x`` raises ``ValueError`` and
+    ``np.diff(level.pos)`` works. This is a zero-copy alias of the device buffer with the
+    same two behaviours: item assignment raises, ``np.asarray`` returns a read-only host
+    copy. Torch operations see a plain tensor (``__torch_function__`` is disabled, so
+    there is no Python overhead and their results are ordinary tensors); the kernels take
+    its ``data_ptr`` as before.
+    """
+
+    __torch_function__ = torch._C._disabled_torch_function_impl
+
+    def __setitem__(self, key, value):
+        raise ValueError("assignment destination is read-only (tensor storage is immutable)")
+
+    def __array__(self, dtype=None, copy=None):
+        a = torch.Tensor.numpy(self.detach().cpu())
+        if dtype is not None:
+            a = a.astype(dtype, copy=False)
+        a.flags.writeable = False
+        return a
+
+
+def _frozen(t: torch.Tensor) -> torch.Tensor:
+    return t if type(t) is StorageArray or not isinstance(t, torch.Tensor) else t.as_subclass(StorageArray)
+
+
 @dataclass(frozen=True)
 class DenseLevel:
     extent: int
@@ -62,12 +91,19 @@ class CompressedLevel:
     pos: torch.Tensor
     crd: torch.Tensor
 
+    def __post_init__(self):
+        object.__setattr__(self, "pos", _frozen(self.pos))
+        object.__setattr__(self, "crd", _frozen(self.crd))
+
 
 @dataclass(frozen=True, eq=False)
 class CoordinateLevel:
     """One column of the aligned coordinate table, int32 on device."""
 
     crd: torch.Tensor
+
+    def __post_init__(self):
+        object.__setattr__(self, "crd", _frozen(self.crd))
 
 
 LevelData = DenseLevel | CompressedLevel | CoordinateLevel
@@ -78,6 +114,9 @@ class TensorStorage:
     format: TensorFormat
     levels: tuple
     values: torch.Tensor
+
+    def __post_init__(self):
+        object.__setattr__(self, "values", _frozen(self.values))
 
     @property
     def device(self) -> torch.device:
