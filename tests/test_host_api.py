@@ -338,3 +338,26 @@ def test_build_from_entries_scalar_and_exact_duplicate_sum():
     t = st.build_from_entries((2, 3), st.csr(2, 3), [((0, 1), 1e16), ((0, 1), 1.0), ((0, 1), -1e16), ((1, 2), 5.0)],
                               device="cpu")
     assert st.to_dense(t)[0, 1] == 1.0 and st.nnz(t) == 2
+
+
+def test_storage_buffers_are_read_only_and_numpy_convertible():
+    """Level and value buffers behave like the reference's frozen arrays (tensor.py:53-56,
+    71-72): assignment raises ValueError, numpy sees a read-only copy; torch ops on them
+    return ordinary tensors and the buffers alias the device memory (no copy)."""
+    import torch
+
+    from paper_2405_16883_b200.tensor import StorageArray
+
+    t = st.from_dense(np.array([[1.0, 0, 2], [0, 3, 0]]), st.csr(2, 3), name="T", device="cpu")
+    lv = t.storage.levels[1]
+    for buf in (lv.pos, lv.crd, t.storage.values):
+        assert type(buf) is StorageArray
+        with pytest.raises(ValueError):
+            buf[0] = 1
+        a = np.asarray(buf)
+        assert not a.flags.writeable and np.array_equal(a, buf.numpy())
+    assert np.array_equal(np.diff(lv.pos), [2, 1]) and lv.pos[-1] == st.nnz(t)
+    assert type(t.storage.values * 2) is torch.Tensor and type(t.storage.values[1:]) is torch.Tensor
+    c = st.convert(t, st.coo(2, 3))
+    assert type(c.storage.values) is StorageArray
+    assert np.array_equal(st.to_dense(c), st.to_dense(t))
