@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/stc.h"
 
 namespace stc {
@@ -32,6 +34,17 @@ inline int check_launch(const char* what) {
   set_error_message("");
   return STC_OK;
 }
+
+// NVTX range around one C-ABI call (header-only NVTX v3: a no-op unless a profiler injects
+// itself), named after the entry point and, for SpMM, the variant -- nsys / ncu --nvtx group
+// the launches by the reference operation they replace.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define STC_NVTX(name) ::stc::NvtxRange stc_nvtx_range_(name)
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

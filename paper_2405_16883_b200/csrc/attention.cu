@@ -51,6 +51,7 @@ extern "C" int stc_sddmm_csr_f32(int m, int n, int d, int heads, const int* rowp
                                  const float* maskvals, long long nnz, const float* Q, long long q_hs,
                                  long long q_rs, const float* K, long long k_hs, long long k_rs, float scale,
                                  float* out_vals, void* stream) {
+  STC_NVTX("stc_sddmm_csr_f32");
   int rc = check_common(m, n, d, heads, rowptr, nnz);
   if (rc) return rc;
   if (m == 0 || nnz == 0) return STC_OK;
@@ -77,6 +78,7 @@ extern "C" int stc_sddmm_csr_f32(int m, int n, int d, int heads, const int* rowp
 
 extern "C" int stc_segsoftmax_csr_f32(int m, int heads, const int* rowptr, long long nnz, float* vals,
                                       void* stream) {
+  STC_NVTX("stc_segsoftmax_csr_f32");
   int rc = check_common(m, 0, 0, heads, rowptr, nnz);
   if (rc) return rc;
   if (m == 0 || nnz == 0) return STC_OK;
@@ -91,6 +93,7 @@ extern "C" int stc_sparse_attention_f32(int m, int n, int d, int heads, const in
                                         long long q_rs, const float* K, long long k_hs, long long k_rs,
                                         const float* V, long long v_hs, long long v_rs, float scale, float* O,
                                         long long o_hs, long long o_rs, float* S, float* P, void* stream) {
+  STC_NVTX("stc_sparse_attention_f32");
   int rc = check_common(m, n, d, heads, rowptr, nnz);
   if (rc) return rc;
   if (m == 0) return STC_OK;
@@ -125,6 +128,7 @@ extern "C" int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, in
                                               long long k_hs, long long k_rs, const float* V, long long v_hs,
                                               long long v_rs, float scale, float* O, long long o_hs, long long o_rs,
                                               void* ws, size_t ws_bytes, void* stream) {
+  STC_NVTX("stc_sparse_attention_tiled_f32");
   int rc = check_common(m, n, d, heads, rem_rowptr, rem_nnz);
   if (rc) return rc;
   if (m == 0) return STC_OK;

@@ -94,6 +94,7 @@ __global__ void fsum_segments_kernel(long long n_seg, const long long* __restric
 
 extern "C" int stc_fsum_segments_f64(long long n_seg, const long long* starts, const double* vals, double* out,
                                      void* stream) {
+  STC_NVTX("stc_fsum_segments_f64");
   if (n_seg < 0) return stc::fail(STC_EINVAL, "negative segment count");
   if (n_seg == 0) return STC_OK;
   if (!starts || !vals || !out) return stc::fail(STC_EINVAL, "null pointer");

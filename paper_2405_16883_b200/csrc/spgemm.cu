@@ -357,6 +357,7 @@ extern "C" size_t stc_spgemm_products_temp_bytes(int m) {
 
 extern "C" int stc_spgemm_products(int m, const int* a_rowptr, const int* a_colidx, const int* b_rowptr,
                                    long long* prod_ptr, void* temp, size_t temp_bytes, void* stream) {
+  STC_NVTX("stc_spgemm_products");
   if (m < 0) return fail(STC_EINVAL, "negative extent");
   if (!a_rowptr || !b_rowptr || !prod_ptr) return fail(STC_EINVAL, "null pointer");
   const size_t need = stc_spgemm_products_temp_bytes(m);
@@ -423,6 +424,7 @@ extern "C" int stc_spgemm_symbolic(int m, int p, const int* a_rowptr, const int*
                                    const int* b_rowptr, const int* b_colidx, const float* b_vals,
                                    const long long* prod_ptr, long long products, void* ws, size_t ws_bytes,
                                    int* c_rowptr, void* stream) {
+  STC_NVTX("stc_spgemm_symbolic");
   if (m < 0 || p < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
   if (!a_rowptr || !b_rowptr || !prod_ptr || !c_rowptr || !ws) return fail(STC_EINVAL, "null pointer");
   const size_t need = stc_spgemm_workspace_bytes(m, p, products);
@@ -465,6 +467,7 @@ extern "C" int stc_spgemm_numeric(int m, int p, const int* a_rowptr, const int* 
                                   const int* b_rowptr, const int* b_colidx, const float* b_vals, long long products,
                                   void* ws, size_t ws_bytes, const int* c_rowptr, int* c_colidx, float* c_vals,
                                   void* stream) {
+  STC_NVTX("stc_spgemm_numeric");
   if (m < 0 || p < 0 || products < 0) return fail(STC_EINVAL, "negative extent");
   if (!ws || !c_rowptr) return fail(STC_EINVAL, "null pointer");
   const size_t need = stc_spgemm_workspace_bytes(m, p, products);
@@ -489,6 +492,7 @@ extern "C" size_t stc_csr_ewise_temp_bytes(int m) {
 extern "C" int stc_csr_ewise_symbolic(int op, int m, const int* a_rowptr, const int* a_colidx, const int* b_rowptr,
                                       const int* b_colidx, int* c_rowptr, void* temp, size_t temp_bytes,
                                       void* stream) {
+  STC_NVTX("stc_csr_ewise_symbolic");
   if (op != STC_EWISE_UNION && op != STC_EWISE_INTERSECT) return fail(STC_EINVAL, "unknown element-wise op %d", op);
   if (m < 0) return fail(STC_EINVAL, "negative extent");
   if (!a_rowptr || !b_rowptr || !c_rowptr) return fail(STC_EINVAL, "null pointer");
@@ -510,6 +514,7 @@ extern "C" int stc_csr_ewise_symbolic(int op, int m, const int* a_rowptr, const 
 extern "C" int stc_csr_ewise_f32(int op, int m, const int* a_rowptr, const int* a_colidx, const float* a_vals,
                                  const int* b_rowptr, const int* b_colidx, const float* b_vals, const int* c_rowptr,
                                  int* c_colidx, float* c_vals, void* stream) {
+  STC_NVTX("stc_csr_ewise_f32");
   if (op != STC_EWISE_UNION && op != STC_EWISE_INTERSECT) return fail(STC_EINVAL, "unknown element-wise op %d", op);
   if (m < 0) return fail(STC_EINVAL, "negative extent");
   if (!a_rowptr || !b_rowptr || !c_rowptr) return fail(STC_EINVAL, "null pointer");

@@ -61,6 +61,8 @@ int spmm_common(int batch, int m, int n, int k, const int* rowptr, const int* co
                 long long nnz, long long val_bs, const float* B, long long ldb, long long b_bs, float* C,
                 long long ldc, long long c_bs, const float* D, long long ldd, int variant, int epilogue,
                 const int* partition, int ipg, void* ws, size_t ws_bytes, void* stream) {
+  STC_NVTX(variant == STC_VARIANT_COLTILE ? "stc_spmm/coltile"
+           : variant == STC_VARIANT_MERGE ? "stc_spmm/merge" : "stc_spmm/row");
   if (m < 0 || n < 0 || k < 0 || nnz < 0 || batch < 1) return fail(STC_EINVAL, "negative extent");
   if (nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "nnz exceeds int32 index range");
   if (m == 0 || k == 0) return STC_OK;
@@ -202,6 +204,7 @@ extern "C" long long stc_coltile_plan_ints(int m, int n, long long nnz) {
 
 extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, const int* colidx,
                                 const float* vals, int* plan, long long plan_ints, void* stream) {
+  STC_NVTX("stc_coltile_plan");
   if (m < 0 || n < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
   if (!plan || !rowptr || (nnz && (!colidx || !vals))) return fail(STC_EINVAL, "null pointer");
   if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_CHUNK) * CTT_ROWS + 1 >= INT32_MAX)
@@ -260,6 +263,7 @@ __global__ void merge_interleave_kernel(int m, long long nnz, const int* __restr
 
 extern "C" int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* colidx, const float* vals,
                                     int span, int* colidx_out, float* vals_out, void* stream) {
+  STC_NVTX("stc_merge_interleave");
   if (m < 0 || nnz < 0 || span < 1) return fail(STC_EINVAL, "bad interleave arguments");
   if (m == 0 || nnz == 0) return STC_OK;
   if (!rowptr || !colidx || !vals || !colidx_out || !vals_out) return fail(STC_EINVAL, "null pointer");
@@ -276,6 +280,7 @@ extern "C" long long stc_merge_path_groups(int m, long long nnz, int items_per_g
 
 extern "C" int stc_merge_path_partition(int m, long long nnz, const int* rowptr, int items_per_group,
                                         int* starts, void* stream) {
+  STC_NVTX("stc_merge_path_partition");
   if (m < 0 || nnz < 0 || items_per_group < 1) return fail(STC_EINVAL, "bad partition arguments");
   if (!rowptr || !starts) return fail(STC_EINVAL, "null pointer");
   if (((uintptr_t)starts & 7u) != 0) return fail(STC_EINVAL, "starts must be 8-byte aligned");
@@ -344,6 +349,7 @@ extern "C" size_t stc_coo_segments_temp_bytes(long long nnz) {
 
 extern "C" int stc_coo_segments(long long nnz, const int* rows, int* seg_rows, int* seg_ptr, int* n_seg_out,
                                 void* temp, size_t temp_bytes, void* stream) {
+  STC_NVTX("stc_coo_segments");
   if (nnz < 0 || nnz > INT32_MAX) return fail(STC_EUNSUPPORTED, "bad nnz");
   if (!seg_ptr || !n_seg_out || (nnz && (!rows || !seg_rows))) return fail(STC_EINVAL, "null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -428,6 +434,7 @@ extern "C" int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, cons
                                    int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
                                    const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                                    void* stream) {
+  STC_NVTX("stc_mttkrp_coo3_f32");
   return mttkrp_common(n_seg, rank, seg_ptr, jcrd, kcrd, vals, nnz, n_j, B, ldb, n_k, C, ldcf, M, ldm, variant,
                        partition, items_per_group, ws, ws_bytes, stream);
 }
