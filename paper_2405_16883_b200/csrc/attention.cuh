@@ -198,10 +198,8 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
 #pragma unroll
     for (int t = 0; t < B; ++t) {
       const float pt = __shfl_sync(mask, p, t, G);
-      o.x = fmaf(pt, vv[t].x, o.x);
-      o.y = fmaf(pt, vv[t].y, o.y);
-      o.z = fmaf(pt, vv[t].z, o.z);
-      o.w = fmaf(pt, vv[t].w, o.w);
+      fma2(o.x, o.y, pt, vv[t].x, vv[t].y);  // packed FMAs (FFMA2), same roundings
+      fma2(o.z, o.w, pt, vv[t].z, vv[t].w);
     }
     run_max = new_max;
   }

@@ -53,8 +53,13 @@ struct TileArgs {
 // four CTAs fit an SM and cover each other's copies). K rows are stored with
 // their 16-byte chunks XOR-swizzled by (row / 4) % 8 and P^T with its row chunks
 // swizzled the same way, so the 8 lanes of a quarter-warp hit 8 bank groups.
+// Round 2: both products issue packed FMAs (FFMA2, stc_common.cuh). Q is staged
+// transposed once per block (Qt[d][row]) so one LDS.128 yields four rows of a head
+// dim: S accumulates as row pairs (S[i], S[i+1]) += (Qt[d][i], Qt[d][i+1]) * K[c][d],
+// and O as head-dim pairs (O[e], O[e+1]) += P[i] * (V[c][e], V[c][e+1]) — 76 issue
+// slots per 128 FMAs instead of 140, every sum in the same order as before.
 // ---------------------------------------------------------------------------
-constexpr size_t AT8_SMEM = 3ull * AT_B * AT_B * sizeof(float);  // Qs, Ks (aliased by Pt), Vs
+constexpr size_t AT8_SMEM = 3ull * AT_B * AT_B * sizeof(float);  // Qt, Ks (aliased by Pt), Vs
 
 // TXN threads share a row: TXN = 8 -> 8x8 register tiles (64 threads), TXN = 16 -> 8x4 (128 threads).
 // Column / head-dim j of thread tx: (j / 4) * 4 * TXN + 4 * tx + j % 4.
@@ -67,8 +72,8 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
   constexpr int NT = 8 * TXN;   // threads
   constexpr int CW = 64 / TXN;  // columns (and head dims) per thread
   extern __shared__ __align__(16) float sm8[];
-  float* Qs = sm8;                  // [row][d]
-  float* Ks = Qs + AT_B * AT_B;     // [col][d], chunk-swizzled
+  float* Qt = sm8;                  // [d][row] (transposed once per block)
+  float* Ks = Qt + AT_B * AT_B;     // [col][d], chunk-swizzled
   float* Vs = Ks + AT_B * AT_B;     // [col][d]
   float* Pt = Ks;                   // [col][row], row-chunk swizzled (K is dead once S is done)
   const int b = blockIdx.x, h = blockIdx.y;
@@ -93,10 +98,19 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
   int n_t = 0;
   while (n_t < a.dt_max && cols[n_t] >= 0) ++n_t;
   for (int t = 0; t < n_t; ++t) STC_CHECK(cols[t] * AT_B < a.n, "dense tile outside the key range");
-  stage_rows(Qs, Qh, a.q_rs, row0, a.m, false);
   if (n_t > 0) {
     stage_rows(Ks, Kh, a.k_rs, cols[0] * AT_B, a.n, true);
     stage_rows(Vs, Vh, a.v_rs, cols[0] * AT_B, a.n, false);
+  }
+  // Q^T: lane = row (conflict-free transposed stores), 16 bytes of a row per load
+  for (int idx = tid; idx < AT_B * 16; idx += NT) {
+    const int r = idx % AT_B, dq = idx / AT_B;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row0 + r < a.m) q = *reinterpret_cast<const float4*>(Qh + (long long)(row0 + r) * a.q_rs + dq * 4);
+    Qt[(4 * dq + 0) * AT_B + r] = q.x;
+    Qt[(4 * dq + 1) * AT_B + r] = q.y;
+    Qt[(4 * dq + 2) * AT_B + r] = q.z;
+    Qt[(4 * dq + 3) * AT_B + r] = q.w;
   }
 
   float o[8][CW], mrow[8], lrow[8];
@@ -109,7 +123,7 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
   }
 
   for (int t = 0; t < n_t; ++t) {
-    cp_async_wait<1>();  // Q and K(t) landed; V(t) may still be in flight
+    cp_async_wait<1>();  // K(t) landed; V(t) may still be in flight (Q^T: plain stores, same barrier)
     __syncthreads();
     float s[8][CW];
 #pragma unroll
@@ -118,23 +132,25 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
       for (int j = 0; j < CW; ++j) s[i][j] = 0.f;
 #pragma unroll 1
     for (int dq = 0; dq < 16; ++dq) {
-      float4 q4[8], k4[CW];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) q4[i] = *reinterpret_cast<const float4*>(Qs + at8_row(ty, i) * AT_D + dq * 4);
+      float4 k4[CW];
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
         const int c = at8_col<TXN>(tx, j);
         k4[j] = *reinterpret_cast<const float4*>(Ks + c * AT_D + ((dq ^ ((c >> 2) & 7)) * 4));
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int dd = 0; dd < 4; ++dd) {  // head dim d = 4 dq + dd, ascending as before
+        const float4 qa = *reinterpret_cast<const float4*>(Qt + (4 * dq + dd) * AT_B + 4 * ty);
+        const float4 qb = *reinterpret_cast<const float4*>(Qt + (4 * dq + dd) * AT_B + 32 + 4 * ty);
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          s[i][j] = fmaf(q4[i].x, k4[j].x, s[i][j]);
-          s[i][j] = fmaf(q4[i].y, k4[j].y, s[i][j]);
-          s[i][j] = fmaf(q4[i].z, k4[j].z, s[i][j]);
-          s[i][j] = fmaf(q4[i].w, k4[j].w, s[i][j]);
+          const float kd = dd == 0 ? k4[j].x : dd == 1 ? k4[j].y : dd == 2 ? k4[j].z : k4[j].w;
+          fma2(s[0][j], s[1][j], kd, qa.x, qa.y);
+          fma2(s[2][j], s[3][j], kd, qa.z, qa.w);
+          fma2(s[4][j], s[5][j], kd, qb.x, qb.y);
+          fma2(s[6][j], s[7][j], kd, qb.z, qb.w);
         }
+      }
     }
     __syncthreads();  // every warp is done with Ks: P^T takes its place
 
@@ -206,14 +222,13 @@ __global__ void __launch_bounds__(8 * TXN, 4) attn_tile8_kernel(TileArgs a) {
           v8[4 * eq] = v4.x; v8[4 * eq + 1] = v4.y; v8[4 * eq + 2] = v4.z; v8[4 * eq + 3] = v4.w;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int e = 0; e < CW; ++e) {
-            if constexpr (decltype(masked)::value)
-              o[i][e] = signbit(p8[i]) ? o[i][e] : fmaf(p8[i], v8[e], o[i][e]);
-            else
-              o[i][e] = fmaf(p8[i], v8[e], o[i][e]);
+        for (int i = 0; i < 8; ++i) {
+          if constexpr (decltype(masked)::value) {
+            if (signbit(p8[i])) continue;
           }
+#pragma unroll
+          for (int e = 0; e < CW; e += 2) fma2(o[i][e], o[i][e + 1], p8[i], v8[e], v8[e + 1]);
+        }
       }
     };
     if (v_finite)

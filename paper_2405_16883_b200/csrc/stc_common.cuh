@@ -85,6 +85,63 @@ STC_DEVICE void st_stream1(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// ---- packed fp32 arithmetic (sm_100a: PTX *.f32x2 -> SASS FFMA2 / FMUL2) ---------
+// One issue slot for two IEEE fp32 operations on an aligned register pair; each half is
+// exactly fma.rn.f32 / mul.rn.f32, so results are bit-identical to the scalar forms. The
+// FP32 pipe spends two cycles on a packed op (tools/ffma2_probe.cu: 117.8 against 124.7
+// FMA/clk/SM), so this buys issue slots, not flops: it pays in the kernels that are bound by
+// instruction issue (COLTILE, the tiled attention kernel, the MTTKRP loop).
+// ptxas folds the b64 packing moves into register allocation when the halves already sit in
+// an aligned pair (float4 loads, tcgen05.ld quads) and uses the scalar-broadcast form of
+// FFMA2 when both halves of a multiplicand are the same register.
+#ifndef STC_NO_PACKED_FMA
+#define STC_PACKED_FMA 1
+#else
+#define STC_PACKED_FMA 0
+#endif
+
+// (d0, d1) = a * (b0, b1) + (d0, d1)
+STC_DEVICE void fma2(float& d0, float& d1, float a, float b0, float b1) {
+#if STC_PACKED_FMA
+  uint64_t av, bv, dv;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bv) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(dv) : "f"(d0), "f"(d1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dv) : "l"(av), "l"(bv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(dv));
+#else
+  d0 = fmaf(a, b0, d0);
+  d1 = fmaf(a, b1, d1);
+#endif
+}
+// (d0, d1) = (a0, a1) * (b0, b1) + (d0, d1)
+STC_DEVICE void fma2v(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+#if STC_PACKED_FMA
+  uint64_t av, bv, dv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(av) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bv) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(dv) : "f"(d0), "f"(d1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dv) : "l"(av), "l"(bv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(dv));
+#else
+  d0 = fmaf(a0, b0, d0);
+  d1 = fmaf(a1, b1, d1);
+#endif
+}
+// (d0, d1) = a * (b0, b1)
+STC_DEVICE void mul2(float& d0, float& d1, float a, float b0, float b1) {
+#if STC_PACKED_FMA
+  uint64_t av, bv, dv;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bv) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(dv) : "l"(av), "l"(bv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(dv));
+#else
+  d0 = a * b0;
+  d1 = a * b1;
+#endif
+}
+
 // ---- VEC-wide register fragments ------------------------------------------------
 
 template <int VEC>
