@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define STC_ABI_VERSION 2  /* 2: L2-persisting entry points removed, stc_fsum_segments_f64 added */
+#define STC_ABI_VERSION 3  /* 2: L2-persisting entry points removed, stc_fsum_segments_f64 added; 3: prepared-item MTTKRP */
 
 #define STC_OK 0
 #define STC_EINVAL (-1)       /* null / misaligned pointer, bad shape        */
@@ -197,6 +197,26 @@ int stc_mttkrp_coo3_f32(int n_seg, int rank, const int* seg_ptr, const int* jcrd
                         int n_k, const float* C, long long ldcf, float* M, long long ldm, int variant,
                         const int* partition, int items_per_group, void* ws, size_t ws_bytes,
                         void* stream);
+
+/* Prepared form of the same contraction (ABI 3). `stc_mttkrp_prepare_items` rewrites the
+ * entry streams once, at plan time, as 16-byte items {element offset of B[j,:], element
+ * offset of C[k,:], T, first-entry-of-an-(i,j)-fiber flag} for the given leading dimensions
+ * (`items`: stc_mttkrp_items_bytes(nnz) bytes, 16-byte aligned; 32-bit offsets, so factors
+ * below 2^32 elements). `stc_mttkrp_coo3_prepared_f32` then runs the merge-path reduction
+ * with the items streamed through small per-group circular buffers by cp.async (no staging
+ * round trips, and the SM keeps its L1 for the factor rows): same partition format, workspace
+ * (stc_spmm_workspace_bytes with the MERGE variant), summation order and results as
+ * stc_mttkrp_coo3_f32 with STC_VARIANT_MERGE. Call it with the ldb / ldcf the items were
+ * prepared for; `stc_mttkrp_prepared_items_per_group` plans the partition granularity for
+ * its kernel. Replaces the same loop nest, engine.py:577-644.                               */
+size_t stc_mttkrp_items_bytes(long long nnz);
+int stc_mttkrp_prepare_items(long long nnz, const int* jcrd, const int* kcrd, const float* vals, int n_j,
+                             long long ldb, int n_k, long long ldcf, void* items, void* stream);
+int stc_mttkrp_prepared_items_per_group(int n_seg, long long nnz, int rank);
+int stc_mttkrp_coo3_prepared_f32(int n_seg, int rank, const int* seg_ptr, const void* items, long long nnz,
+                                 int n_j, const float* B, long long ldb, int n_k, const float* C,
+                                 long long ldcf, float* M, long long ldm, const int* partition,
+                                 int items_per_group, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- device-side construction --------------------------
  * Exact duplicate folding: out[s] = fsum(vals[starts[s] .. starts[s+1])), the correctly

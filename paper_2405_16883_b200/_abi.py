@@ -77,6 +77,11 @@ SIGNATURES = {
                                             _ll, _p, _ll, _ll, _f, _p, _ll, _ll, _p, _sz, _p]),
     "stc_mttkrp_coo3_f32": (_i, [_i, _i, _p, _p, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _i, _p, _i,
                                  _p, _sz, _p]),
+    "stc_mttkrp_items_bytes": (_sz, [_ll]),
+    "stc_mttkrp_prepare_items": (_i, [_ll, _p, _p, _p, _i, _ll, _i, _ll, _p, _p]),
+    "stc_mttkrp_prepared_items_per_group": (_i, [_i, _ll, _i]),
+    "stc_mttkrp_coo3_prepared_f32": (_i, [_i, _i, _p, _p, _ll, _i, _p, _ll, _i, _p, _ll, _p, _ll, _p, _i,
+                                          _p, _sz, _p]),
     "stc_fsum_segments_f64": (_i, [_ll, _p, _p, _p, _p]),
     "stc_spgemm_products_temp_bytes": (_sz, [_i]),
     "stc_spgemm_products": (_i, [_i, _p, _p, _p, _p, _p, _sz, _p]),

@@ -17,7 +17,8 @@ LIB = PKG / "libstc.so"
 # checked build: device-side bounds / protocol checks (STC_CHECK) compiled in; for test runs
 # only (tools/run_checked.sh loads it through STC_LIBRARY)
 LIB_CHECKED = PKG / "libstc_checked.so"
-SOURCES = ["abi_common.cu", "spmm.cu", "spmm_wide.cu", "attention.cu", "spgemm.cu", "construct.cu"]
+SOURCES = ["abi_common.cu", "spmm.cu", "spmm_wide.cu", "mttkrp_prepared.cu", "attention.cu", "spgemm.cu",
+           "construct.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

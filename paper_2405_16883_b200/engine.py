@@ -706,8 +706,11 @@ def _exec_mttkrp(ctx: _Ctx, mk: _MttkrpTerm) -> Tensor:
     else:
         jc, kc = st.levels[1].crd, st.levels[2].crd
     variant = ctx.variant if ctx.variant in ("row", "merge") else "merge"
-    part = _cache(view, ("partition", "mttkrp", Bd.shape[1]),
-                  lambda: ops.merge_partition(seg.ptr, st.values.numel(), k=Bd.shape[1], kind="mttkrp")) \
+    fkey = (Bd.shape[0], Bd.stride(0), Cd.shape[0], Cd.stride(0))
+    # the plan holds the entries as prepared items for these factor shapes (jc/kc swapped with B/C above)
+    part = _cache(view, ("partition", "mttkrp", Bd.shape[1], mk.b_first, fkey),
+                  lambda: ops.merge_partition(seg.ptr, st.values.numel(), k=Bd.shape[1], kind="mttkrp",
+                                              jcrd=jc, kcrd=kc, vals=st.values, factors=fkey)) \
         if variant == "merge" else None
     M = ops.mttkrp_coo3(seg, jc, kc, st.values, Bd, Cd, variant=variant, partition=part)
     ctx.chosen.append(f"mttkrp:{variant}")

@@ -25,6 +25,8 @@ DEFAULT_ITEMS_PER_GROUP = int(os.environ.get("STC_ITEMS_PER_GROUP", "0"))
 MERGE_SKEW_THRESHOLD = 8.0
 # Interleave the entries of rows longer than a merge group (plans built with colidx/vals).
 INTERLEAVE = os.environ.get("STC_INTERLEAVE", "1") != "0"
+# MTTKRP plans carry prepared items (cp.async-staged kernel); 0 = raw-stream merge kernel (A/B runs)
+PREPARED_MTTKRP = os.environ.get("STC_PREPARED_MTTKRP", "1") != "0"
 # Dense widths above which the column-tiled variant is chosen.
 COLTILE_MIN_K = 512
 
@@ -109,6 +111,11 @@ class MergePartition:
     m: int = -1               # rows and entries of the structure the plan was built for
     nnz: int = -1
     source: tuple | None = None   # (data_ptr, _version) of the colidx / vals the copies came from
+    # MTTKRP plans built with the tensor's (jcrd, kcrd, vals) and the factors' shapes: the
+    # entries as prepared 16-byte items (stc_mttkrp_prepare_items) for `items_key` =
+    # (n_j, ldb, n_k, ldc); mttkrp_coo3 then runs the cp.async-staged kernel.
+    items: torch.Tensor | None = None
+    items_key: tuple | None = None
     _ws: dict = field(default_factory=dict, repr=False)
 
     def check(self, m: int, nnz: int, colidx: torch.Tensor, vals: torch.Tensor) -> None:
@@ -157,7 +164,10 @@ def interleave_long_rows(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch
 
 
 def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "spmm") -> int:
-    ipg = int(lib().stc_merge_plan_items_per_group(m, nnz, max(k, 1), batch, 1 if kind == "mttkrp" else 0))
+    if kind == "mttkrp_prepared":
+        ipg = int(lib().stc_mttkrp_prepared_items_per_group(m, nnz, max(k, 1)))
+    else:
+        ipg = int(lib().stc_merge_plan_items_per_group(m, nnz, max(k, 1), batch, 1 if kind == "mttkrp" else 0))
     if ipg < 0:
         check(ipg, "stc_merge_plan_items_per_group")
     return ipg
@@ -166,15 +176,24 @@ def plan_items_per_group(m: int, nnz: int, k: int, batch: int = 1, kind: str = "
 @on_operand_device
 def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None = None, *,
                     k: int = 128, batch: int = 1, kind: str = "spmm", colidx: torch.Tensor | None = None,
-                    vals: torch.Tensor | None = None, max_row: int | None = None) -> MergePartition:
+                    vals: torch.Tensor | None = None, max_row: int | None = None,
+                    jcrd: torch.Tensor | None = None, kcrd: torch.Tensor | None = None,
+                    factors: tuple | None = None) -> MergePartition:
     """Plan-time merge-path partition; ``items_per_group`` None/0 = planned for ``k``.
     With the matrix's ``colidx``/``vals`` (SpMM) the plan also carries their long-row
-    interleaved copies, and ``spmm_csr`` reads those; use such a plan only with that matrix."""
+    interleaved copies, and ``spmm_csr`` reads those; use such a plan only with that matrix.
+    ``kind="mttkrp"`` with the tensor's ``jcrd``/``kcrd``/``vals`` and ``factors`` =
+    (n_j, ldb, n_k, ldc) also prepares the entries as 16-byte items for the cp.async-staged
+    MTTKRP kernel (a 16-byte-per-entry copy of T for those leading dimensions)."""
     require_cuda(rowptr)
     _i32(rowptr)
     m = rowptr.numel() - 1
+    prepared = (kind == "mttkrp" and PREPARED_MTTKRP and jcrd is not None and kcrd is not None
+                and vals is not None and factors is not None and nnz > 0
+                and (factors[0] + 1) * factors[1] < 2**32 and (factors[2] + 1) * factors[3] < 2**32)
     if not items_per_group:
-        items_per_group = DEFAULT_ITEMS_PER_GROUP or plan_items_per_group(m, nnz, k, batch, kind)
+        items_per_group = DEFAULT_ITEMS_PER_GROUP or plan_items_per_group(
+            m, nnz, k, batch, "mttkrp_prepared" if prepared else kind)
     groups = int(lib().stc_merge_path_groups(m, nnz, items_per_group))
     starts = torch.empty(2 * (groups + 1), dtype=torch.int32, device=rowptr.device)
     rc = lib().stc_merge_path_partition(m, nnz, ptr(rowptr), items_per_group, ptr(starts),
@@ -187,7 +206,16 @@ def merge_partition(rowptr: torch.Tensor, nnz: int, items_per_group: int | None 
         if max_row > items_per_group:  # some row spans several groups: interleave (a copy of A)
             ci, va = interleave_long_rows(rowptr, _i32(colidx), _f32(vals), items_per_group)
             source = _buffer_id(colidx, vals)
-    return MergePartition(starts, items_per_group, groups, ci, va, m, int(nnz), source)
+    items = items_key = None
+    if prepared:
+        require_cuda(jcrd, kcrd, vals)
+        n_j, ldb, n_k, ldc = (int(x) for x in factors)
+        items = torch.empty(int(lib().stc_mttkrp_items_bytes(nnz)), dtype=torch.uint8, device=rowptr.device)
+        check(lib().stc_mttkrp_prepare_items(nnz, ptr(_i32(jcrd)), ptr(_i32(kcrd)), ptr(_f32(vals)), n_j, ldb,
+                                             n_k, ldc, ptr(items), stream_handle()), "stc_mttkrp_prepare_items")
+        items_key = (n_j, ldb, n_k, ldc)
+        source = (jcrd.data_ptr(), jcrd._version, kcrd.data_ptr(), kcrd._version, vals.data_ptr(), vals._version)
+    return MergePartition(starts, items_per_group, groups, ci, va, m, int(nnz), source, items, items_key)
 
 
 @dataclass
@@ -543,14 +571,31 @@ def mttkrp_coo3(seg: Segments, jcrd, kcrd, vals, B: torch.Tensor, C: torch.Tenso
     n_seg = seg.n_seg
     M = torch.empty((n_seg, R), dtype=torch.float32, device=B.device)
     ipg = 0
+    key = (B.shape[0], B.stride(0), C.shape[0], C.stride(0))
     if variant == "merge":
-        partition = partition or merge_partition(seg.ptr, nnz, k=R, kind="mttkrp")
+        partition = partition or merge_partition(seg.ptr, nnz, k=R, kind="mttkrp", jcrd=jcrd, kcrd=kcrd,
+                                                 vals=vals, factors=key)
         if (partition.m, partition.nnz) != (n_seg, nnz):
             raise ValueError(f"merge partition built for m={partition.m}, nnz={partition.nnz}")
         ipg = partition.items_per_group
         if workspace is None:
             workspace = partition.workspace(R, 1, B.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
+    if variant == "merge" and partition.items is not None:
+        # prepared items: the plan's copy of T for these leading dimensions
+        if partition.items_key != key:
+            raise ValueError(f"MTTKRP plan prepared for factors (n_j, ldb, n_k, ldc) = {partition.items_key}, "
+                             f"called with {key}: rebuild it with merge_partition(..., factors=...)")
+        if partition.source != (jcrd.data_ptr(), jcrd._version, kcrd.data_ptr(), kcrd._version,
+                                vals.data_ptr(), vals._version):
+            raise ValueError("MTTKRP plan carries prepared items of other coordinate / value buffers "
+                             "(or of values modified since): rebuild it")
+        rc = lib().stc_mttkrp_coo3_prepared_f32(
+            n_seg, R, ptr(seg.ptr), ptr(partition.items), nnz, B.shape[0], ptr(B), B.stride(0), C.shape[0],
+            ptr(C), C.stride(0), ptr(M), M.stride(0), ptr(partition.starts), ipg, ptr(workspace), ws_bytes,
+            stream_handle())
+        check(rc, "stc_mttkrp_coo3_prepared_f32")
+        return M
     rc = lib().stc_mttkrp_coo3_f32(
         n_seg, R, ptr(seg.ptr), ptr(jcrd), ptr(kcrd), ptr(vals), nnz, B.shape[0], ptr(B), B.stride(0),
         C.shape[0], ptr(C), C.stride(0), ptr(M), M.stride(0), _abi.VARIANTS[variant],

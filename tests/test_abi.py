@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_only_entry_points():
     lib = _abi.load_library()
-    assert lib.stc_abi_version() == 2
+    assert lib.stc_abi_version() == 3
     assert lib.stc_last_error() == b""
     assert lib.stc_merge_path_groups(10, 30, 8) == 7   # 2 items per row end + 1 per entry: ceil(50 / 8)
     assert lib.stc_merge_path_groups(0, 0, 8) == 0
@@ -60,6 +60,19 @@ def test_argument_validation_without_gpu():
     rc = lib.stc_merge_interleave(4, 10, None, 8, 8, 64, 16, 16, None)   # null rowptr
     assert rc == _abi.STC_EINVAL and b"null" in lib.stc_last_error()
     assert lib.stc_merge_interleave(0, 0, None, None, None, 64, None, None, None) == _abi.STC_OK  # empty
+    # prepared-item MTTKRP (ABI 3)
+    assert lib.stc_mttkrp_items_bytes(10) == 160 and lib.stc_mttkrp_items_bytes(-1) == 0
+    rc = lib.stc_mttkrp_prepare_items(5, 8, 8, 8, 1 << 27, 32, 10, 32, 16, None)   # offsets need 33 bits
+    assert rc == _abi.STC_EUNSUPPORTED and b"32-bit" in lib.stc_last_error()
+    rc = lib.stc_mttkrp_prepare_items(5, 8, 8, 8, 10, 32, 10, 32, 8, None)         # items not 16-byte aligned
+    assert rc == _abi.STC_EINVAL and b"aligned" in lib.stc_last_error()
+    assert lib.stc_mttkrp_prepare_items(0, None, None, None, 10, 32, 10, 32, None, None) == _abi.STC_OK
+    rc = lib.stc_mttkrp_coo3_prepared_f32(4, 32, 8, 16, 5, 10, 16, 32, 10, 16, 32, 16, 32, None, 64, None, 0, None)
+    assert rc == _abi.STC_EINVAL and b"partition" in lib.stc_last_error()
+    rc = lib.stc_mttkrp_coo3_prepared_f32(4, 32, 8, 16, 5, 10, 16, 16, 10, 16, 32, 16, 32, 16, 64, None, 0, None)
+    assert rc == _abi.STC_EINVAL and b"leading dimension" in lib.stc_last_error()
+    rc = lib.stc_mttkrp_coo3_prepared_f32(4, 32, 8, 16, 5, 10, 16, 32, 10, 16, 32, 16, 32, 16, 64, None, 0, None)
+    assert rc == _abi.STC_EWORKSPACE
     rc = lib.stc_sddmm_csr_f32(4, 4, 48, 1, 8, 8, None, 4, 16, 0, 48, 16, 0, 48, 1.0, 32, None)
     assert rc == _abi.STC_EUNSUPPORTED
     with pytest.raises(ValueError):

@@ -223,6 +223,72 @@ def test_coo_segments_and_mttkrp():
             assert parity_gate(got, want[:, :R], want[:, :R], TOL)[0]
 
 
+def _zipf_coo3(seed, dim, draws):
+    rng = np.random.default_rng(seed)
+    i = np.minimum(rng.zipf(1.3, draws) - 1, dim - 1)
+    j = np.minimum(rng.zipf(1.2, draws) - 1, dim - 1)
+    k = rng.integers(0, dim, draws)
+    key = np.unique((i * dim + j) * dim + k)
+    i, j, k = key // (dim * dim), (key // dim) % dim, key % dim
+    vals = rng.uniform(0, 1, len(key)).astype(np.float32)
+    return rng, i, j, k, vals
+
+
+@pytest.mark.parametrize("R", [4, 7, 32, 64, 128])
+@pytest.mark.parametrize("ipg", [None, 1, 2, 3, 9, 33, 250, 1000])
+def test_mttkrp_prepared_items_matches_raw_kernel_and_oracle(R, ipg):
+    """The cp.async-staged kernel over prepared items (stc_mttkrp_coo3_prepared_f32): bit-identical
+    to the raw-stream merge kernel on the same partition, and within the gate of the oracle — at
+    every group size (carries inside and across CTAs, groups that start mid-fiber, empty groups)."""
+    dim = 400
+    rng, i, j, k, vals = _zipf_coo3(77 + R, dim, 30000)
+    B = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    C = rng.uniform(-1, 1, (dim, R)).astype(np.float32)
+    seg = ops.coo_segments(torch.from_numpy(i).int().cuda())
+    _, ptr_ref = restate.coo_segments(i)
+    Jt, Kt, Vt = torch.from_numpy(j).int().cuda(), torch.from_numpy(k).int().cuda(), torch.from_numpy(vals).cuda()
+    Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
+    fkey = (dim, Bt.stride(0), dim, Ct.stride(0))
+    prep = ops.merge_partition(seg.ptr, len(vals), ipg, k=R, kind="mttkrp", jcrd=Jt, kcrd=Kt, vals=Vt, factors=fkey)
+    assert prep.items is not None and prep.items.numel() == 16 * len(vals)
+    raw = ops.merge_partition(seg.ptr, len(vals), prep.items_per_group, k=R, kind="mttkrp")
+    assert raw.items is None
+    got = ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=prep)
+    ref = ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=raw)
+    assert torch.equal(got, ref)
+    for _ in range(3):  # arrival counters back at zero: relaunches are bit-stable
+        assert torch.equal(ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=prep), got)
+    want = native.mttkrp(ptr_ref, j, k, vals, B, C)
+    bound = native.mttkrp(ptr_ref, j, k, vals, np.abs(B), np.abs(C))
+    assert parity_gate(got.cpu().numpy(), want, bound, TOL)[0]
+
+
+def test_mttkrp_prepared_plan_is_bound_to_its_buffers_and_factor_shapes():
+    dim, R = 50, 32
+    rng, i, j, k, vals = _zipf_coo3(5, dim, 2000)
+    seg = ops.coo_segments(torch.from_numpy(i).int().cuda())
+    Jt, Kt, Vt = torch.from_numpy(j).int().cuda(), torch.from_numpy(k).int().cuda(), torch.from_numpy(vals).cuda()
+    Bt = torch.from_numpy(rng.uniform(0, 1, (dim, R)).astype(np.float32)).cuda()
+    Ct = torch.from_numpy(rng.uniform(0, 1, (dim, R)).astype(np.float32)).cuda()
+    part = ops.merge_partition(seg.ptr, len(vals), k=R, kind="mttkrp", jcrd=Jt, kcrd=Kt, vals=Vt,
+                               factors=(dim, R, dim, R))
+    M0 = ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part)
+    # default call (no plan given) prepares the same way
+    assert torch.equal(ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct), M0)
+    wide = torch.zeros((dim, 2 * R), device="cuda")
+    wide[:, :R] = Bt
+    with pytest.raises(ValueError, match="prepared for factors"):
+        ops.mttkrp_coo3(seg, Jt, Kt, Vt, wide[:, :R], Ct, partition=part)   # ldb = 64: other offsets
+    with pytest.raises(ValueError, match="prepared items of other"):
+        ops.mttkrp_coo3(seg, Jt, Kt, Vt.clone(), Bt, Ct, partition=part)
+    Vt.mul_(2.0)                                                              # values modified in place
+    with pytest.raises(ValueError, match="prepared items of other"):
+        ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part)
+    # strided factor: a fresh plan for its leading dimension
+    got = ops.mttkrp_coo3(seg, Jt, Kt, Vt, wide[:, :R], Ct)
+    assert torch.allclose(got, 2.0 * M0, rtol=1e-6, atol=0)
+
+
 @pytest.mark.parametrize("seq,window,nrand,heads", [(200, 40, 8, 2), (700, 256, 64, 1), (130, 300, 5, 3)])
 def test_tiled_attention_matches_oracle(seq, window, nrand, heads):
     from paper_2405_16883_b200 import synthetic

@@ -181,7 +181,8 @@ def cfg5():
     Vt = torch.from_numpy(vals).cuda()
     seg = ops.coo_segments(It)
     Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
-    part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp")
+    part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp", jcrd=Jt, kcrd=Kt, vals=Vt,
+                               factors=(Bt.shape[0], Bt.stride(0), Ct.shape[0], Ct.stride(0)))
     ws = ops.spmm_workspace(seg.n_seg, len(vals), 32, "merge", part.items_per_group, 1, "cuda")
     ms = gpu_time(lambda: ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part, workspace=ws))
     nnz = len(vals)
@@ -193,7 +194,8 @@ def cfg5():
     v64, b64, c64 = vals.astype(np.float64), B.astype(np.float64), C.astype(np.float64)
     cs = cpu_time(lambda: native.mttkrp(ptr, j, k, v64, b64, c64))
     return record("cfg5_mttkrp_zipf_coo3", ms, flops, nbytes, "hbm", cs, "full",
-                  {"nnz": nnz, "items_per_group": part.items_per_group, "row0_nnz": int(ptr[1])})
+                  {"nnz": nnz, "items_per_group": part.items_per_group, "row0_nnz": int(ptr[1]),
+                   "kernel": "prepared items, cp.async-staged" if part.items is not None else "raw streams"})
 
 
 def spgemm_cfg1():
@@ -271,7 +273,7 @@ def mttkrp_mode2_cfg5():
     view = T._cache[("mttkrp_view", (1, 0, 2))]
     vst = view.storage
     seg = view._cache[("coo_segments",)]
-    part = view._cache[("partition", "mttkrp", 32)]
+    part = next(v for kk, v in view._cache.items() if kk[:3] == ("partition", "mttkrp", 32))
     Bd, Cd = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
     ms = gpu_time(lambda: ops.mttkrp_coo3(seg, vst.levels[1].crd, vst.levels[2].crd, vst.values, Bd, Cd,
                                           partition=part))

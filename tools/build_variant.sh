@@ -4,7 +4,7 @@ name=$1; shift
 mkdir -p ab/$name.obj
 P=paper_2405_16883_b200
 pids=()
-for src in abi_common spmm spmm_wide attention spgemm construct; do
+for src in abi_common spmm spmm_wide mttkrp_prepared attention spgemm construct; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" \
     -I include -c $P/csrc/$src.cu -o ab/$name.obj/$src.o &
   pids+=($!)

@@ -14,7 +14,8 @@ def cfg5():
     Vt = torch.from_numpy(vals).cuda()
     seg = ops.coo_segments(It)
     Bt, Ct = torch.from_numpy(B).cuda(), torch.from_numpy(C).cuda()
-    part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp")
+    part = ops.merge_partition(seg.ptr, len(vals), k=32, kind="mttkrp", jcrd=Jt, kcrd=Kt, vals=Vt,
+                               factors=(Bt.shape[0], Bt.stride(0), Ct.shape[0], Ct.stride(0)))
     return lambda: ops.mttkrp_coo3(seg, Jt, Kt, Vt, Bt, Ct, partition=part)
 
 
