@@ -33,6 +33,20 @@ int launch_attn(const AttnArgs& a, cudaStream_t st) {
   return check_launch("attention_kernel");
 }
 
+// the tiled path's remainder pass (d = 64): V rows staged through shared memory by cp.async
+int launch_attn_vsmem(const AttnArgs& a, cudaStream_t st) {
+  constexpr int G = 16;
+  constexpr size_t smem = (size_t)(G / 2) * kThreads * sizeof(float4);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attention_vsmem_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
+  attention_vsmem_kernel<G><<<grid, kThreads, smem, st>>>(a);
+  return check_launch("attention_vsmem_kernel");
+}
+
 template <bool WS>
 int attn_by_d(const AttnArgs& a, cudaStream_t st) {
   switch (a.d / 4) {
@@ -171,5 +185,9 @@ extern "C" int stc_sparse_attention_tiled_f32(int m, int n, int d, int heads, in
   a.O = O; a.o_hs = o_hs; a.o_rs = o_rs;
   a.Opart = t.Opart;
   a.ml = t.ml;
+#ifdef STC_ATTN_NO_VSMEM
   return launch_attn<16, false>(a, st);
+#else
+  return launch_attn_vsmem(a, st);
+#endif
 }

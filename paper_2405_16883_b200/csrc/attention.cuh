@@ -141,9 +141,18 @@ __global__ void __launch_bounds__(256) segsoftmax_kernel(int m, long long nnz, c
 // Fused: O[h,i,:] = sum_j softmax_j(scale * m_ij * q_i.k_j) * v_j with an online softmax.
 // Entries are consumed in batches of B <= G (B = G/2 for wide heads keeps the
 // V-row registers small enough for two CTAs' worth of extra warps per SM).
-template <int G, bool WRITE_S>
-__global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
+// VSMEM (the tiled path's remainder pass): the V rows of a batch do not wait in registers
+// while the scores are reduced — each lane copies its 16-byte slice of every row into its own
+// shared-memory slot with cp.async (no register, no cross-lane traffic: the lane reads back
+// what it copied) and loads it when the probabilities are known. 32 registers fewer per
+// thread: MINB CTAs per SM instead of 3, i.e. more batches of gathers in flight per SM.
+#ifndef STC_ATTN_VSMEM_MINB
+#define STC_ATTN_VSMEM_MINB 4
+#endif
+template <int G, bool WRITE_S, bool VSMEM>
+STC_DEVICE void attention_body(const AttnArgs& a) {
   constexpr int B = G >= 16 ? G / 2 : G;
+  extern __shared__ __align__(16) float4 vstage[];  // VSMEM: [B][256] float4, slot [t][thread]
   const int lane = threadIdx.x % G;
   const unsigned mask = subwarp_mask<G>();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -166,19 +175,22 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     const int n = min(B, end - base);
     const int my_col = next_col;
     float part[B];
-    float4 vv[B];
+    float4 vv[VSMEM ? 1 : B];
 #pragma unroll
     for (int t = 0; t < B; ++t) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
-      vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (!VSMEM) vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
       STC_CHECK(t >= n || (c >= 0 && c < a.n), "attention column outside K/V");
+      if constexpr (VSMEM)  // zero-filled past the row's end
+        cp_async16(&vstage[t * 256 + threadIdx.x], Vh + (long long)(t < n ? c : 0) * a.v_rs, t < n);
       if (t < n) {
         kv = ld_gather4(Kh + (long long)c * a.k_rs);
-        vv[t] = ld_gather4(Vh + (long long)c * a.v_rs);
+        if constexpr (!VSMEM) vv[t] = ld_gather4(Vh + (long long)c * a.v_rs);
       }
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
+    if constexpr (VSMEM) cp_async_commit();
     // indices of the next batch stream in while this one is reduced
     next_col = (base + B + lane < end && lane < B) ? ld_stream(a.colidx + base + B + lane) : 0;
     float s = transpose_reduce_b<B, G>(part, lane, mask);
@@ -195,11 +207,13 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
     // each entry appears in G / B lanes: count it once in the sum
     run_sum = run_sum * corr + group_sum<G>(lane < B ? p : 0.f, mask);
     o.x *= corr; o.y *= corr; o.z *= corr; o.w *= corr;
+    if constexpr (VSMEM) cp_async_wait<0>();  // this thread's own copies: no barrier needed
 #pragma unroll
     for (int t = 0; t < B; ++t) {
       const float pt = __shfl_sync(mask, p, t, G);
-      fma2(o.x, o.y, pt, vv[t].x, vv[t].y);  // packed FMAs (FFMA2), same roundings
-      fma2(o.z, o.w, pt, vv[t].z, vv[t].w);
+      const float4 v = VSMEM ? vstage[t * 256 + threadIdx.x] : vv[t];
+      fma2(o.x, o.y, pt, v.x, v.y);  // packed FMAs (FFMA2), same roundings
+      fma2(o.z, o.w, pt, v.z, v.w);
     }
     run_max = new_max;
   }
@@ -214,6 +228,15 @@ __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
         a.P[h * a.nnz + pp] = expf(a.S[h * a.nnz + pp] - run_max) * inv;
     }
   }
+}
+
+template <int G, bool WRITE_S>
+__global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
+  attention_body<G, WRITE_S, false>(a);
+}
+template <int G>
+__global__ void __launch_bounds__(256, STC_ATTN_VSMEM_MINB) attention_vsmem_kernel(AttnArgs a) {
+  attention_body<G, false, true>(a);
 }
 
 }  // namespace stc
