@@ -2,7 +2,8 @@
 //
 // C[r, c0:c0+128] = sum_p val[p] * B[col[p], c0:c0+128] for a block of 128 rows.
 //
-// Operand path:  global --bulk copy (TMA engine, producer warp)--> SMEM stage (64 B rows x 512 B)
+// Operand path:  global --one tiled TMA copy per chunk (tensor map; producer warp)--> SMEM stage
+//                (63 B rows x 512 B + one all-zero row that padding entries point at)
 //                --LDS.128 + tcgen05.st (each lane quarter's 4 warps)--> TMEM
 //                --tcgen05.ld.32x32b.x4--> registers (lane l: B[j, c0+4l .. c0+4l+3])
 // Each staged row is reused by every row of the block holding that column (~12.8
@@ -22,12 +23,17 @@
 // cuSPARSE SpMM preprocess): rebuild it when the values change.
 //
 // Pipeline (1 CTA/SM, TMEM = 2 buffers x 256 columns):
-//   producer warp  : bulk copies (TMA engine, one per 512-byte B row) of chunk c -> SMEM stage
-//                    c % 3 once all consumers copied chunk c - 3 out of it (mbarrier `sempty`);
-//                    completion by transaction count on mbarrier `sfull`
+//   producer warp  : one cp.async.bulk.tensor.2d (63 x 128 box, zero fill past n / k) of chunk c ->
+//                    SMEM stage c % 3 once all consumers copied chunk c - 3 out of it (mbarrier
+//                    `sempty`); completion by transaction count on mbarrier `sfull`. An operand
+//                    that cannot be mapped (no encoder entry point) falls back to one bulk copy
+//                    per 512-byte row -- 63 of them cost the TMA engine ~2900 cycles per chunk,
+//                    which the consumers waited on (cfg3 4.71 -> 3.84 ms with the tiled copy)
 //   16 consumer    : wait `sfull`, copy their 16 rows of chunk c+1 into their lane quarter,
 //   warps            consume chunk c, then a named barrier per quarter (4 warps)
 #pragma once
+
+#include <cuda.h>  // CUtensorMap (the type only: the encoder is fetched through the runtime, spmm.cu)
 
 #include <type_traits>
 
@@ -35,16 +41,21 @@
 
 namespace stc {
 
+#ifndef CTT_GROUP_UNROLL
+#define CTT_GROUP_UNROLL 2
+#endif
+constexpr int kGroupUnroll = CTT_GROUP_UNROLL;    // groups per unrolled body of a row's loop
 constexpr int CTT_ROWS = 128;
 constexpr int CTT_COLS = 128;
-constexpr int CTT_CHUNK = 64;
+constexpr int CTT_CHUNK = 64;                     // operand slots per chunk in SMEM / TMEM
+constexpr int CTT_BROWS = CTT_CHUNK - 1;          // B rows per chunk; the last slot is an all-zero row
 constexpr int CTT_WARPS = 16;                      // consumer warps; one more warp produces
 constexpr int CTT_THREADS = (CTT_WARPS + 1) * 32;
 constexpr int CTT_STAGES = 3;
 constexpr int CTT_RPW = CTT_ROWS / CTT_WARPS;     // rows per consumer warp
 constexpr int CTT_PAD = 4;                        // row segments padded to this many entries
 constexpr int CTT_ECAP = 128;                     // staged entries per warp and chunk
-constexpr int CTT_PAD_ADDR = -1;                  // TMEM address of a padding entry
+constexpr int CTT_ZERO_SLOT = 4 * CTT_BROWS;      // TMEM column of the zero row inside a chunk's buffer
 constexpr size_t CTT_STAGE_FLOATS = (size_t)CTT_CHUNK * CTT_COLS;
 constexpr size_t CTT_SMEM = CTT_STAGES * CTT_STAGE_FLOATS * sizeof(float)  // B stages
                             + (size_t)CTT_WARPS * 2 * CTT_ECAP * 8          // entry lists (double)
@@ -62,7 +73,7 @@ STC_DEVICE void ctt_mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 // ---- plan -----------------------------------------------------------------------------------
-// chunk_ptr[row * (n_chunks + 1) + c] = first entry of `row` with col >= c * CTT_CHUNK
+// chunk_ptr[row * (n_chunks + 1) + c] = first entry of `row` with col >= c * CTT_BROWS
 __global__ void ctt_chunk_ptr_kernel(int m, int n_chunks, const int* __restrict__ rowptr,
                                      const int* __restrict__ colidx, int* __restrict__ chunk_ptr) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -72,7 +83,7 @@ __global__ void ctt_chunk_ptr_kernel(int m, int n_chunks, const int* __restrict_
   int* out = chunk_ptr + (long long)row * (n_chunks + 1);
   for (int c = lane; c <= n_chunks; c += 32) {
     int lo = a, hi = b;
-    const int key = c * CTT_CHUNK;
+    const int key = c * CTT_BROWS;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (colidx[mid] < key)
@@ -116,10 +127,10 @@ __global__ void ctt_scatter_kernel(int m, int n_chunks, const int* __restrict__ 
     // the entry carries its full TMEM address (the kernel's allocation starts at column 0):
     // lane quarter of the row's consumer warp, TMEM buffer of the chunk, 4 columns per B row
     const int base = ((32 * (((row % CTT_ROWS) / CTT_RPW) % 4)) << 16) + (c & 1) * 4 * CTT_CHUNK;
-    for (int p = a; p < b; ++p) ent[e++] = make_int2(base + 4 * (colidx[p] - c * CTT_CHUNK), __float_as_int(vals[p]));
-    // padding: address -1 marks "no entry" (only a row's last group of 4 holds any; the
-    // kernel skips them there, so 0 * Inf / NaN from an unreferenced B row cannot occur)
-    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(CTT_PAD_ADDR, 0);
+    for (int p = a; p < b; ++p) ent[e++] = make_int2(base + 4 * (colidx[p] - c * CTT_BROWS), __float_as_int(vals[p]));
+    // padding: weight 0 on the chunk's all-zero slot -- 0 * 0, never 0 * Inf / NaN from a B
+    // row the matrix row does not reference, and the kernel needs no tail case
+    for (int q = b - a; q % CTT_PAD; ++q) ent[e++] = make_int2(base + CTT_ZERO_SLOT, 0);
   }
 }
 
@@ -128,7 +139,8 @@ template <int EPI, bool ADD>
 __global__ void __launch_bounds__(CTT_THREADS, 1)
     coltile_tmem_kernel(int m, int n, int k, const int* __restrict__ offs, const int2* __restrict__ ent,
                         const float* __restrict__ B, long long ldb, float* __restrict__ C, long long ldc,
-                        const float* __restrict__ D, long long ldd) {
+                        const float* __restrict__ D, long long ldd, const __grid_constant__ CUtensorMap bmap,
+                        int use_bmap) {
   extern __shared__ __align__(1024) float smem[];
   int2* lists = reinterpret_cast<int2*>(smem + CTT_STAGES * CTT_STAGE_FLOATS);  // [warp][2][ECAP]
   uint64_t* sfull = reinterpret_cast<uint64_t*>(lists + CTT_WARPS * 2 * CTT_ECAP);
@@ -137,8 +149,11 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int c0 = blockIdx.y * CTT_COLS;
-  const int n_chunks = (n + CTT_CHUNK - 1) / CTT_CHUNK;
+  const int n_chunks = (n + CTT_BROWS - 1) / CTT_BROWS;
 
+  // slot 63 of every stage is the zero row: the bulk copies fill slots 0..62 only
+  for (int t = threadIdx.x; t < CTT_STAGES * CTT_COLS; t += CTT_THREADS)
+    smem[(t / CTT_COLS) * CTT_STAGE_FLOATS + (size_t)CTT_BROWS * CTT_COLS + t % CTT_COLS] = 0.f;
   if (warp == 0) {  // TMEM: 512 columns = two 256-column buffers
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(ctt_smem_u32(tbase_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -165,10 +180,29 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
     for (int c = 0; c < n_chunks; ++c) {
       const int s = c % CTT_STAGES;
       if (c >= CTT_STAGES) ctt_mbar_wait(ctt_smem_u32(&sempty[s]), (uint32_t)((c / CTT_STAGES - 1) & 1));
-      const int j0 = c * CTT_CHUNK;
-      const int rows = min(CTT_CHUNK, n - j0);
+      const int j0 = c * CTT_BROWS;
+      const int rows = min(CTT_BROWS, n - j0);
       float* dst = smem + s * CTT_STAGE_FLOATS;
-      if (rows < CTT_CHUNK || row_bytes < 4 * CTT_COLS) {  // zero what the copies do not cover
+      if (use_bmap) {
+        // one tiled copy per chunk: the 63 x 128 box of B at (row j0, column c0); rows past n and
+        // columns past k arrive as zeros and count towards the transaction bytes. (63 row copies
+        // of 512 bytes keep the TMA engine busy ~2900 cycles per chunk, longer than the
+        // consumers need for it: the consumers waited on `sfull` for 18 % of their samples.)
+        if (lane == 0) {
+          const uint32_t bar = ctt_smem_u32(&sfull[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"((uint32_t)(CTT_BROWS * CTT_COLS * sizeof(float)))
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                  ctt_smem_u32(dst)),
+              "l"(&bmap), "r"(c0), "r"(j0), "r"(bar)
+              : "memory");
+        }
+        __syncwarp();
+        continue;
+      }
+      if (rows < CTT_BROWS || row_bytes < 4 * CTT_COLS) {  // zero what the copies do not cover
         for (int idx = lane; idx < (int)(CTT_STAGE_FLOATS / 4); idx += 32) {
           const int jr = idx / 32, cq = idx % 32;
           if (jr >= rows || 16 * cq >= row_bytes)
@@ -258,40 +292,35 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
     float acc[CTT_RPW][4];
 #pragma unroll
     for (int r = 0; r < CTT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
-    // 4 entries -> 4 tcgen05.ld, one wait, 16 FFMA. TAIL: a row's last group, whose padding
-    // entries (address CTT_PAD_ADDR) load a valid address and leave the accumulators alone.
-    auto group = [&](float (&a)[4], int4 e01, int4 e23, auto tail) {
-      constexpr bool TAIL = decltype(tail)::value;
+    // 4 entries -> 4 tcgen05.ld, one wait, 8 packed FMAs (padding entries: weight 0 on the zero slot)
+    auto group = [&](float (&a)[4], int4 e01, int4 e23) {
       uint32_t x[4][4];
-      int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
-      bool pad[4] = {false, false, false, false};
+      const int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if constexpr (TAIL) {
-          pad[u] = taddr[u] == CTT_PAD_ADDR;
-          taddr[u] = pad[u] ? (int)tq : taddr[u];
-        }
+      for (int u = 0; u < 4; ++u)
         STC_CHECK((uint32_t)taddr[u] >> 16 == 32u * quarter && (taddr[u] & 0xffff) < 512,
                   "COLTILE entry outside the warp's TMEM lane quarter");
-      }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
                      : "r"(taddr[u]));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // the loaded registers pass through the wait, so no use of them can be scheduled above it
+      asm volatile("tcgen05.wait::ld.sync.aligned;"
+                   : "+r"(x[0][0]), "+r"(x[0][1]), "+r"(x[0][2]), "+r"(x[0][3]), "+r"(x[1][0]), "+r"(x[1][1]),
+                     "+r"(x[1][2]), "+r"(x[1][3]), "+r"(x[2][0]), "+r"(x[2][1]), "+r"(x[2][2]), "+r"(x[2][3]),
+                     "+r"(x[3][0]), "+r"(x[3][1]), "+r"(x[3][2]), "+r"(x[3][3])
+                   :
+                   : "memory");
       const float w[4] = {__int_as_float(e01.y), __int_as_float(e01.w), __int_as_float(e23.y),
                           __int_as_float(e23.w)};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (TAIL && pad[u]) continue;
         // packed FMAs (FFMA2, value broadcast): 8 issue slots per group instead of 16
         fma2(a[0], a[1], w[u], __uint_as_float(x[u][0]), __uint_as_float(x[u][1]));
         fma2(a[2], a[3], w[u], __uint_as_float(x[u][2]), __uint_as_float(x[u][3]));
       }
     };
-    using Body = std::false_type;
-    using Tail = std::true_type;
 
     int meta = load_meta(0);
     int meta_next = load_meta(1);
@@ -313,32 +342,24 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
       };
       const int e0 = __shfl_sync(0xffffffffu, meta, 0);
       const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
-      if (total <= CTT_ECAP) {
-        const int4* sc = reinterpret_cast<const int4*>(mylists + (ch & 1) * CTT_ECAP);
+      STC_CHECK(total >= 0 && total % CTT_PAD == 0, "COLTILE chunk list length");
+      // lane r: groups of row r in this chunk; the rows' groups are contiguous in the list, so one
+      // pointer walks it (chunks denser than the staged list read it straight from global memory)
+      const int ngrp = (__shfl_down_sync(0xffffffffu, meta, 1) - meta) / CTT_PAD;
+      auto rows = [&](const int4* gp) {
 #pragma unroll
         for (int r = 0; r < CTT_RPW; ++r) {
-          const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
-          const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
+          const int nr = __shfl_sync(0xffffffffu, ngrp, r);
           fill_step(r);
-          STC_CHECK(qa <= qb && qb <= total, "COLTILE row list outside the staged chunk list");
-          if (qb > qa) {
-            for (int q = qa; q < qb - CTT_PAD; q += CTT_PAD) group(acc[r], sc[q / 2], sc[q / 2 + 1], Body{});
-            group(acc[r], sc[(qb - CTT_PAD) / 2], sc[(qb - CTT_PAD) / 2 + 1], Tail{});
-          }
+          STC_CHECK(nr >= 0 && nr * CTT_PAD <= total, "COLTILE row list outside the chunk list");
+#pragma unroll kGroupUnroll
+          for (int g = 0; g < nr; ++g, gp += 2) group(acc[r], gp[0], gp[1]);
         }
-      } else {  // rows denser than the staged list: entries straight from global memory
-        const int4* g = reinterpret_cast<const int4*>(ent + e0);
-#pragma unroll
-        for (int r = 0; r < CTT_RPW; ++r) {
-          const int qa = __shfl_sync(0xffffffffu, meta, r) - e0;
-          const int qb = __shfl_sync(0xffffffffu, meta, r + 1) - e0;
-          fill_step(r);
-          if (qb > qa) {
-            for (int q = qa; q < qb - CTT_PAD; q += CTT_PAD) group(acc[r], g[q / 2], g[q / 2 + 1], Body{});
-            group(acc[r], g[(qb - CTT_PAD) / 2], g[(qb - CTT_PAD) / 2 + 1], Tail{});
-          }
-        }
-      }
+      };
+      if (total <= CTT_ECAP)
+        rows(reinterpret_cast<const int4*>(mylists + (ch & 1) * CTT_ECAP));  // LDS
+      else
+        rows(reinterpret_cast<const int4*>(ent + e0));                       // LDG
       if (next) {
         fill_store(ch + 1, kPhases - 1);
         __syncwarp();

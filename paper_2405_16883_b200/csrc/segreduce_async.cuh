@@ -46,20 +46,42 @@ struct MttkrpItemsOp {
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
     STC_CHECK(!it.flag || (unsigned long long)(it.offb + lane_off) + VEC <= limitb, "MTTKRP gather outside B");
     STC_CHECK((unsigned long long)(it.offc + lane_off) + VEC <= limitc, "MTTKRP gather outside C");
+#ifdef STC_MTTKRP_COLDHOT
+    // experiment: rows the plan marked cold (flag bits 1 / 2) are gathered without an L1 allocation,
+    // so the in-flight misses do not push the hot factor rows out of the L1
+    if (it.flag & 1) {
+      if (it.flag & 4) pre.b.load_stream(B + (it.offb + lane_off));
+      else pre.b.load_gather(B + (it.offb + lane_off));
+    }
+    if (it.flag & 2) pre.c.load_stream(C + (it.offc + lane_off));
+    else pre.c.load_gather(C + (it.offc + lane_off));
+#else
     if (it.flag) pre.b.load_gather(B + (it.offb + lane_off));
     pre.c.load_gather(C + (it.offc + lane_off));
+#endif
   }
   STC_DEVICE static void init(State& st) { st.b.zero(); }
   STC_DEVICE void accumulate(Frag<VEC>& acc, State& st, const Pre& pre, const Item& it) const {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      st.b.v[e] = it.flag ? pre.b.v[e] : st.b.v[e];
-      acc.v[e] = fmaf(it.v * st.b.v[e], pre.c.v[e], acc.v[e]);
+    for (int e = 0; e < VEC; ++e) st.b.v[e] = (it.flag & 1) ? pre.b.v[e] : st.b.v[e];
+#ifdef STC_MTTKRP_F2
+    if constexpr (VEC % 2 == 0) {
+      // packed halves: each is exactly mul.rn / fma.rn, so the sums do not change
+#pragma unroll
+      for (int e = 0; e < VEC; e += 2) {
+        float t0, t1;
+        mul2(t0, t1, it.v, st.b.v[e], st.b.v[e + 1]);
+        fma2v(acc.v[e], acc.v[e + 1], t0, t1, pre.c.v[e], pre.c.v[e + 1]);
+      }
+      return;
     }
+#endif
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc.v[e] = fmaf(it.v * st.b.v[e], pre.c.v[e], acc.v[e]);
   }
   STC_DEVICE static void finish(Frag<VEC>&, State&) {}
   // a group starts mid-fiber: its first entry must load B[j,:] whatever the stored flag says
-  STC_DEVICE static void mark_first(Item& it) { it.flag = 1; }
+  STC_DEVICE static void mark_first(Item& it) { it.flag |= 1; }
 };
 
 // Plan-time item build: one thread per entry.
@@ -71,12 +93,19 @@ __global__ void mttkrp_items_kernel(long long nnz, const int* __restrict__ jc, c
        p += (long long)gridDim.x * blockDim.x) {
     const int j = jc[p];
     const bool start = p == 0 || jc[p - 1] != j;
-    items[p] = Item{(unsigned)((long long)j * ldb), (unsigned)((long long)kc[p] * ldcf), val[p], start ? 1 : 0};
+    int flag = start ? 1 : 0;
+#ifdef STC_MTTKRP_COLDHOT
+    if (kc[p] >= STC_MTTKRP_COLDHOT) flag |= 2;
+    if (j >= STC_MTTKRP_COLDHOT) flag |= 4;
+#endif
+    items[p] = Item{(unsigned)((long long)j * ldb), (unsigned)((long long)kc[p] * ldcf), val[p], flag};
   }
 }
 
+// 8-entry chunks (16 KB of item rings per CTA) against 16 (32 KB): cfg5 116.8 -> 110.6 us -- the L1 the
+// rings leave is what keeps the hot factor rows resident under ~1000 in-flight gather lines per SM
 #ifndef STC_ASYNC_CHUNK
-#define STC_ASYNC_CHUNK 16
+#define STC_ASYNC_CHUNK 8
 #endif
 template <int SUBW>
 __host__ __device__ constexpr int async_chunk() {
@@ -91,7 +120,20 @@ template <int SUBW, class Op>
 __host__ __device__ constexpr int async_item_stride() {
   return bank_skewed(async_ring_items<SUBW, Op>(), (int)sizeof(typename Op::Item));
 }
-constexpr int kAsyncRows = 32;  // staged row ends per group (restaged when a group owns more)
+#ifndef STC_ASYNC_UNROLL
+#define STC_ASYNC_UNROLL 0
+#endif
+template <int W, int U>
+__host__ __device__ constexpr int async_unroll() {
+  // entries per unrolled body of the chunk loop (0: the whole chunk)
+  return STC_ASYNC_UNROLL > 0 && STC_ASYNC_UNROLL < W && STC_ASYNC_UNROLL % U == 0 && W % STC_ASYNC_UNROLL == 0
+             ? STC_ASYNC_UNROLL
+             : W;
+}
+#ifndef STC_ASYNC_ROWS
+#define STC_ASYNC_ROWS 32
+#endif
+constexpr int kAsyncRows = STC_ASYNC_ROWS;  // staged row ends per group (restaged when a group owns more)
 template <int SUBW, int VEC, class Op>
 __host__ __device__ constexpr size_t merge_async_smem_bytes() {
   constexpr int NG = 256 / SUBW;
@@ -229,14 +271,27 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_async_kernel(SegOut
     const int cw = c * W;
     end_w = cur_end - cw;
     if (cw + W <= n_nnz) {  // full chunk: W / U ring turns, entry t + U lies in this chunk or the next
+      // unrolled F entries at a time (F a multiple of the ring depth, so ring slots stay
+      // static): the fully unrolled chunk with its inlined flush paths is ~25 k SASS lines
+      // and stalls on instruction fetch (no_instruction 9 % of samples at F = W = 16)
+      constexpr int F = async_unroll<W, U>();
+#pragma unroll 1
+      for (int tb = 0; tb < W; tb += F) {
 #pragma unroll
-      for (int t = 0; t < W; ++t) {
-        while (t >= end_w) {
-          flush();
-          end_w = cur_end - cw;
+        for (int q = 0; q < F; ++q) {
+          const int t = tb + q;
+          while (t >= end_w) {
+            flush();
+            end_w = cur_end - cw;
+          }
+          op.accumulate(acc, fst, ring[q % U], cur[t]);
+          if (col_ok) {
+            if constexpr (F == W)
+              op.fetch(t + U < W ? cur[t + U] : nxt[t + U - W], ring[q % U]);
+            else
+              op.fetch(items[(cw + t + U) & (RING - 1)], ring[q % U]);
+          }
         }
-        op.accumulate(acc, fst, ring[t % U], cur[t]);
-        if (col_ok) op.fetch(t + U < W ? cur[t + U] : nxt[t + U - W], ring[t % U]);
       }
     } else if (cw < n_nnz) {  // the group's last, partial chunk (items past the range are zero: harmless gathers)
       const int left = n_nnz - cw;

@@ -1,6 +1,8 @@
 // C-ABI entry points for the segmented gather-reduce family:
 // CSR SpMM (ROW / MERGE / COLTILE), batched CSR SpMM, COO SpMM, MTTKRP,
 // plus the plan-time merge-path partition and COO row segmentation.
+#include <cstdlib>
+
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -24,7 +26,7 @@ struct CttLayout {
 };
 inline CttLayout ctt_layout(int m, int n, long long nnz) {
   CttLayout l{};
-  l.n_chunks = (int)ceil_div(n, CTT_CHUNK);
+  l.n_chunks = (int)ceil_div(n, CTT_BROWS);
   l.n_slots = ceil_div(m, CTT_ROWS) * l.n_chunks * CTT_ROWS;
   l.max_entries = nnz + (long long)(CTT_PAD - 1) * std::min<long long>(nnz, (long long)m * l.n_chunks);
   size_t tb = 0;
@@ -40,6 +42,35 @@ inline CttLayout ctt_layout(int m, int n, long long nnz) {
   return l;
 }
 
+// Tiled tensor map of the dense operand for the COLTILE producer: fp32 [n rows, k columns], row
+// pitch ldb, box = CTT_BROWS rows x CTT_COLS columns, out-of-range elements read as zero. The
+// encoder is a driver entry point fetched through the runtime (the library does not link libcuda,
+// so it still loads on a machine without a driver). False when the operand does not meet the
+// tensor-map alignment rules (16-byte base and pitch) -- the kernel then copies row by row.
+bool ctt_operand_map(const float* B, long long ldb, int n, int k, CUtensorMap* map) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode || n <= 0 || k <= 0) return false;
+  if (const char* e = std::getenv("STC_COLTILE_ROW_COPIES"); e && *e == '1') return false;  // tests: the other path
+  if (reinterpret_cast<uintptr_t>(B) % 16 || (ldb * 4) % 16 || ldb * 4 >= (1LL << 40)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)n};
+  const cuuint64_t pitch[1] = {(cuuint64_t)ldb * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)CTT_COLS, (cuuint32_t)CTT_BROWS};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, pitch, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int EPI, bool ADD>
 int launch_coltile_tmem(int m, int n, int k, long long nnz, const int* plan, const float* B, long long ldb, float* C,
                         long long ldc, const float* D, long long ldd, cudaStream_t st, const Launch& L) {
@@ -51,8 +82,10 @@ int launch_coltile_tmem(int m, int n, int k, long long nnz, const int* plan, con
   if (m == 0 || k == 0) return STC_OK;
   const CttLayout lay = ctt_layout(m, n, nnz);
   const dim3 grid((unsigned)ceil_div(m, CTT_ROWS), (unsigned)ceil_div(k, CTT_COLS));
+  CUtensorMap bmap{};
+  const int use_bmap = ctt_operand_map(B, ldb, n, k, &bmap) ? 1 : 0;
   coltile_tmem_kernel<EPI, ADD><<<grid, dim3(CTT_THREADS), CTT_SMEM, st>>>(
-      m, n, k, plan + lay.offs, reinterpret_cast<const int2*>(plan + lay.ent), B, ldb, C, ldc, D, ldd);
+      m, n, k, plan + lay.offs, reinterpret_cast<const int2*>(plan + lay.ent), B, ldb, C, ldc, D, ldd, bmap, use_bmap);
   return check_launch("coltile_tmem_kernel");
 }
 
@@ -196,7 +229,7 @@ extern "C" int stc_merge_plan_items_per_group(int m, long long nnz, int k, int b
 
 extern "C" long long stc_coltile_plan_ints(int m, int n, long long nnz) {
   if (m < 0 || n < 0 || nnz < 0) return -1;
-  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_CHUNK) * CTT_ROWS + 1 >= INT32_MAX) return -1;
+  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_BROWS) * CTT_ROWS + 1 >= INT32_MAX) return -1;
   const CttLayout lay = ctt_layout(m, n, nnz);
   if (lay.max_entries >= INT32_MAX) return -1;
   return lay.total_ints;
@@ -207,8 +240,8 @@ extern "C" int stc_coltile_plan(int m, int n, long long nnz, const int* rowptr, 
   STC_NVTX("stc_coltile_plan");
   if (m < 0 || n < 0 || nnz < 0) return fail(STC_EINVAL, "negative extent");
   if (!plan || !rowptr || (nnz && (!colidx || !vals))) return fail(STC_EINVAL, "null pointer");
-  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_CHUNK) * CTT_ROWS + 1 >= INT32_MAX)
-    return fail(STC_EUNSUPPORTED, "COLTILE plan: m * ceil(n / 64) slots exceed int32");
+  if ((long long)ceil_div(m, CTT_ROWS) * ceil_div(n, CTT_BROWS) * CTT_ROWS + 1 >= INT32_MAX)
+    return fail(STC_EUNSUPPORTED, "COLTILE plan: m * ceil(n / 63) slots exceed int32");
   const CttLayout lay = ctt_layout(m, n, nnz);
   if (lay.max_entries >= INT32_MAX) return fail(STC_EUNSUPPORTED, "COLTILE plan exceeds int32 entries");
   if (plan_ints < lay.total_ints)

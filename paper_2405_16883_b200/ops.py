@@ -87,14 +87,14 @@ def choose_variant(stats: RowStats, k: int, aligned: bool = True, n_cols: int | 
 
 def coltile_fits(stats: RowStats, n_cols: int | None) -> bool:
     """COLTILE pays off (and its plan is addressable) for this matrix: density at least
-    1/128 and m * ceil(n / 64) plan slots below 2^31. Without ``n_cols`` (unknown width)
+    1/128 and m * ceil(n / 63) plan slots below 2^31. Without ``n_cols`` (unknown width)
     only the density against the widest possible square operand is not checked."""
     if n_cols is None:
         return True
     m = stats.m
     if m == 0 or n_cols == 0:
         return False
-    if m * (-(-n_cols // 64)) >= 2**31 - 1:
+    if m * (-(-n_cols // 63)) >= 2**31 - 1:
         return False
     return stats.nnz * 128 >= m * n_cols
 

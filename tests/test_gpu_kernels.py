@@ -449,6 +449,32 @@ def test_coltile_padding_ignores_nonfinite_unreferenced_rows():
     assert np.array_equal(np.isnan(got), np.isnan(want)) and np.array_equal(np.isinf(got), np.isinf(want))
 
 
+@pytest.mark.parametrize("shape", [(300, 200, 128), (130, 1000, 260), (128, 63, 4), (64, 127, 132)])
+def test_coltile_operand_paths_agree(shape, monkeypatch):
+    """The COLTILE producer stages B by one tiled TMA copy per 63-row chunk (tensor map, zero fill
+    past n and k) or, when the operand cannot be mapped, by one bulk copy per row: both must give
+    the same bits (same plan, same summation order), ragged edges included."""
+    m, n, k = shape
+    rng = np.random.default_rng(m * 7 + n)
+    rp, ci, v = make_csr(rng, m, n, rng.integers(0, min(n, 40), m))
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    R, C, V = dev(rp, ci, v)
+    Bt = torch.from_numpy(B).cuda()
+    tiled = ops.spmm_csr(R, C, V, Bt, variant="coltile")
+    monkeypatch.setenv("STC_COLTILE_ROW_COPIES", "1")
+    by_row = ops.spmm_csr(R, C, V, Bt, variant="coltile")
+    monkeypatch.delenv("STC_COLTILE_ROW_COPIES")
+    assert torch.equal(tiled, by_row)
+    want = native.spmm_csr(rp, ci, v, B)
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B))
+    assert parity_gate(tiled.cpu().numpy(), want, bound, TOL)[0]
+    # a column slice of a wider operand: pitch != width, base offset by 4 floats
+    wide = torch.from_numpy(rng.uniform(-1, 1, (n, k + 8)).astype(np.float32)).cuda()
+    view = wide[:, 4:4 + k]
+    got = ops.spmm_csr(R, C, V, view, variant="coltile")
+    assert torch.equal(got, ops.spmm_csr(R, C, V, view.contiguous(), variant="coltile"))
+
+
 def test_tiled_attention_ignores_nonfinite_unreferenced_value_rows():
     """Dense 64x64 tiles hold absent slots; a V row that some rows of the block do not
     reference may be Inf / NaN without touching those rows (rows that reference it do)."""
