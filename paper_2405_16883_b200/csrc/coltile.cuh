@@ -2,10 +2,10 @@
 //
 // C[r, c0:c0+128] = sum_p val[p] * B[col[p], c0:c0+128] for a block of 128 rows.
 //
-// Operand path:  global --one tiled TMA copy per chunk (tensor map; producer warp)--> SMEM stage
-//                (63 B rows x 512 B + one all-zero row that padding entries point at)
-//                --LDS.128 + tcgen05.st (each lane quarter's 4 warps)--> TMEM
-//                --tcgen05.ld.32x32b.x4--> registers (lane l: B[j, c0+4l .. c0+4l+3])
+// Operand path:  global --one tiled TMA copy per chunk (tensor map)--> SMEM stage (63 B rows x
+//                512 B + one all-zero row that padding entries point at)
+//                --LDS.128 + tcgen05.st (one fill warp per TMEM lane quarter)--> TMEM
+//                --tcgen05.ld.32x32b.x4 (16 consumer warps)--> registers (lane l: B[j, c0+4l .. c0+4l+3])
 // Each staged row is reused by every row of the block holding that column (~12.8
 // at 10 % density). Reading the operand from TMEM takes it off the SMEM crossbar,
 // which caps an SMEM-staged kernel near a quarter of the FP32 peak (the previous
@@ -22,15 +22,20 @@
 // The plan carries the VALUES of A (it is the prepared form of the matrix, like a
 // cuSPARSE SpMM preprocess): rebuild it when the values change.
 //
-// Pipeline (1 CTA/SM, TMEM = 2 buffers x 256 columns):
-//   producer warp  : one cp.async.bulk.tensor.2d (63 x 128 box, zero fill past n / k) of chunk c ->
-//                    SMEM stage c % 3 once all consumers copied chunk c - 3 out of it (mbarrier
-//                    `sempty`); completion by transaction count on mbarrier `sfull`. An operand
-//                    that cannot be mapped (no encoder entry point) falls back to one bulk copy
-//                    per 512-byte row -- 63 of them cost the TMA engine ~2900 cycles per chunk,
-//                    which the consumers waited on (cfg3 4.71 -> 3.84 ms with the tiled copy)
-//   16 consumer    : wait `sfull`, copy their 16 rows of chunk c+1 into their lane quarter,
-//   warps            consume chunk c, then a named barrier per quarter (4 warps)
+// Pipeline (1 CTA/SM, 640 threads, TMEM = 2 buffers x 256 columns, all hand-offs by mbarrier):
+//   fill warp q    : (q = 0 also issues the TMA copies, two chunks ahead: one
+//   (4 warps)        cp.async.bulk.tensor.2d, 63 x 128 box, zero fill past n / k, into stage c % 3
+//                    once all four fill warps have left chunk c - 1's stage -- `sempty`; an operand
+//                    that cannot be mapped falls back to one bulk copy per 512-byte row, 63 of
+//                    which cost the TMA engine ~2900 cycles per chunk: cfg3 4.71 -> 3.84 ms with
+//                    the tiled copy.) Waits for the stage (`sfull`, transaction bytes) and for its
+//                    quarter's buffer c & 1 to be read (`tfree[q]`), copies the 64 slots into the
+//                    quarter (LDS.128 -> tcgen05.st), then arrives on `tfull[q]` and `sempty`.
+//   16 consumer    : wait `tfull[quarter]`, consume chunk c from TMEM, arrive on `tfree[quarter]`.
+//   warps            (Round 2: the consumers used to copy the chunks themselves, interleaved with
+//                    their group loop, and met at a named barrier per quarter: 3.84 -> 3.61 ms.
+//                    tcgen05.cp.32x128b.warpx4 as the copy engine was measured too: ~40 cycles per
+//                    512-byte row during which tcgen05.ld does not proceed -- 5.75 ms.)
 #pragma once
 
 #include <cuda.h>  // CUtensorMap (the type only: the encoder is fetched through the runtime, spmm.cu)
@@ -49,8 +54,9 @@ constexpr int CTT_ROWS = 128;
 constexpr int CTT_COLS = 128;
 constexpr int CTT_CHUNK = 64;                     // operand slots per chunk in SMEM / TMEM
 constexpr int CTT_BROWS = CTT_CHUNK - 1;          // B rows per chunk; the last slot is an all-zero row
-constexpr int CTT_WARPS = 16;                      // consumer warps; one more warp produces
-constexpr int CTT_THREADS = (CTT_WARPS + 1) * 32;
+constexpr int CTT_WARPS = 16;                      // consumer warps
+constexpr int CTT_FILL_WARPS = 4;                  // one per TMEM lane quarter: SMEM stage -> TMEM
+constexpr int CTT_THREADS = (CTT_WARPS + CTT_FILL_WARPS) * 32;  // 640: 96 registers per thread still fit
 constexpr int CTT_STAGES = 3;
 constexpr int CTT_RPW = CTT_ROWS / CTT_WARPS;     // rows per consumer warp
 constexpr int CTT_PAD = 4;                        // row segments padded to this many entries
@@ -59,7 +65,7 @@ constexpr int CTT_ZERO_SLOT = 4 * CTT_BROWS;      // TMEM column of the zero row
 constexpr size_t CTT_STAGE_FLOATS = (size_t)CTT_CHUNK * CTT_COLS;
 constexpr size_t CTT_SMEM = CTT_STAGES * CTT_STAGE_FLOATS * sizeof(float)  // B stages
                             + (size_t)CTT_WARPS * 2 * CTT_ECAP * 8          // entry lists (double)
-                            + 128;                                          // barriers, TMEM address
+                            + 256;                                          // barriers, TMEM address
 
 STC_DEVICE uint32_t ctt_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -143,15 +149,17 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
                         int use_bmap) {
   extern __shared__ __align__(1024) float smem[];
   int2* lists = reinterpret_cast<int2*>(smem + CTT_STAGES * CTT_STAGE_FLOATS);  // [warp][2][ECAP]
-  uint64_t* sfull = reinterpret_cast<uint64_t*>(lists + CTT_WARPS * 2 * CTT_ECAP);
-  uint64_t* sempty = sfull + CTT_STAGES;
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(sempty + CTT_STAGES);
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(lists + CTT_WARPS * 2 * CTT_ECAP);  // stage landed (TMA bytes)
+  uint64_t* sempty = sfull + CTT_STAGES;   // stage copied out by the four fill warps
+  uint64_t* tfull = sempty + CTT_STAGES;   // [quarter][buffer]: TMEM buffer of the quarter written
+  uint64_t* tfree = tfull + 8;             // [quarter][buffer]: ... read by the quarter's four consumer warps
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tfree + 8);
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int c0 = blockIdx.y * CTT_COLS;
   const int n_chunks = (n + CTT_BROWS - 1) / CTT_BROWS;
 
-  // slot 63 of every stage is the zero row: the bulk copies fill slots 0..62 only
+  // slot 63 of every stage is the zero row: the operand copies fill slots 0..62 only
   for (int t = threadIdx.x; t < CTT_STAGES * CTT_COLS; t += CTT_THREADS)
     smem[(t / CTT_COLS) * CTT_STAGE_FLOATS + (size_t)CTT_BROWS * CTT_COLS + t % CTT_COLS] = 0.f;
   if (warp == 0) {  // TMEM: 512 columns = two 256-column buffers
@@ -161,7 +169,11 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < CTT_STAGES; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ctt_smem_u32(&sfull[b])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ctt_smem_u32(&sempty[b])), "r"(CTT_WARPS));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ctt_smem_u32(&sempty[b])), "r"(CTT_FILL_WARPS));
+    }
+    for (int b = 0; b < 8; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ctt_smem_u32(&tfull[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ctt_smem_u32(&tfree[b])), "r"(CTT_WARPS / 4));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -174,22 +186,22 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
   // per-load address add in the inner loop)
   STC_CHECK(tbase == 0u, "TMEM allocation does not start at column 0");
 
-  if (warp == CTT_WARPS) {
-    // ---------------- producer: B chunks -> SMEM stages (bulk copies, one per B row) ----------------
+  if (warp >= CTT_WARPS) {
+    // ---------------- fill warp of lane quarter q ----------------
+    // B chunk c -> SMEM stage c % 3 (TMA, issued by the fill warp of quarter 0, two chunks ahead)
     const int row_bytes = 4 * min(CTT_COLS, k - c0);  // multiple of 16 (k % 4 == 0)
-    for (int c = 0; c < n_chunks; ++c) {
+    auto stage_in = [&](int c) {
       const int s = c % CTT_STAGES;
-      if (c >= CTT_STAGES) ctt_mbar_wait(ctt_smem_u32(&sempty[s]), (uint32_t)((c / CTT_STAGES - 1) & 1));
       const int j0 = c * CTT_BROWS;
       const int rows = min(CTT_BROWS, n - j0);
       float* dst = smem + s * CTT_STAGE_FLOATS;
+      const uint32_t bar = ctt_smem_u32(&sfull[s]);
       if (use_bmap) {
         // one tiled copy per chunk: the 63 x 128 box of B at (row j0, column c0); rows past n and
         // columns past k arrive as zeros and count towards the transaction bytes. (63 row copies
         // of 512 bytes keep the TMA engine busy ~2900 cycles per chunk, longer than the
-        // consumers need for it: the consumers waited on `sfull` for 18 % of their samples.)
+        // consumers need for it: they waited on the stage for 18 % of their samples.)
         if (lane == 0) {
-          const uint32_t bar = ctt_smem_u32(&sfull[s]);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                        "r"((uint32_t)(CTT_BROWS * CTT_COLS * sizeof(float)))
                        : "memory");
@@ -200,17 +212,17 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
               : "memory");
         }
         __syncwarp();
-        continue;
+        return;
       }
       if (rows < CTT_BROWS || row_bytes < 4 * CTT_COLS) {  // zero what the copies do not cover
         for (int idx = lane; idx < (int)(CTT_STAGE_FLOATS / 4); idx += 32) {
           const int jr = idx / 32, cq = idx % 32;
-          if (jr >= rows || 16 * cq >= row_bytes)
+          if (jr < CTT_BROWS && (jr >= rows || 16 * cq >= row_bytes))
             *reinterpret_cast<float4*>(dst + jr * CTT_COLS + cq * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
-      const uint32_t bar = ctt_smem_u32(&sfull[s]);
+      __syncwarp();
       if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rows * row_bytes)
                      : "memory");
@@ -222,12 +234,46 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
                 ctt_smem_u32(dst + jr * CTT_COLS)),
             "l"(B + (long long)(j0 + jr) * ldb + c0), "r"(row_bytes), "r"(bar)
             : "memory");
+      __syncwarp();
+    };
+    // SMEM stage -> TMEM buffer c & 1 of the quarter:
+    // lane l holds B[j, c0 + 4l .. + 3] of every staged row j (LDS.128) and stores it to columns
+    // 4j .. 4j + 3 of its quarter (tcgen05.st); the zero row (slot 63) is copied like the others
+    const int q = warp - CTT_WARPS;  // == warp % 4: the quarter this warp may access
+    const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
+    if (q == 0)
+      for (int c = 0; c < min(CTT_STAGES - 1, n_chunks); ++c) stage_in(c);
+    for (int c = 0; c < n_chunks; ++c) {
+      const int s = c % CTT_STAGES, b = c & 1;
+      if (q == 0 && c + CTT_STAGES - 1 < n_chunks) {  // chunk c + 2 into the stage chunk c - 1 has left
+        if (c >= 1) ctt_mbar_wait(ctt_smem_u32(&sempty[(c - 1) % CTT_STAGES]), (uint32_t)(((c - 1) / CTT_STAGES) & 1));
+        stage_in(c + CTT_STAGES - 1);
+      }
+      if (c >= 2) ctt_mbar_wait(ctt_smem_u32(&tfree[2 * q + b]), (uint32_t)((c / 2 - 1) & 1));  // chunk c - 2 read
+      ctt_mbar_wait(ctt_smem_u32(&sfull[s]), (uint32_t)((c / CTT_STAGES) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float* src = smem + s * CTT_STAGE_FLOATS + lane * 4;
+      const uint32_t dst = tq + (uint32_t)(b * 4 * CTT_CHUNK);
+#pragma unroll 8
+      for (int j = 0; j < CTT_CHUNK; ++j) {  // (unrolled: the loads run ahead of the TMEM stores)
+        const float4 v = *reinterpret_cast<const float4*>(src + j * CTT_COLS);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + 4 * j),
+                     "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+                     "r"(__float_as_uint(v.w))
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&tfull[2 * q + b])) : "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[s])) : "memory");
+      }
     }
   } else {
     // ---------------- consumers: 8 rows x 128 columns each ----------------
     const int row_base = blockIdx.x * CTT_ROWS + warp * CTT_RPW;
-    const int quarter = warp % 4, part = warp / 4;
-    const uint32_t tq = tbase + ((uint32_t)(32 * quarter) << 16);  // this warp's TMEM lane quarter
+    const int quarter = warp % 4;
     int2* mylists = lists + warp * 2 * CTT_ECAP;
     const int* offs_w = offs + (long long)blockIdx.x * n_chunks * CTT_ROWS + warp * CTT_RPW;
     // lanes 0..CTT_RPW: the warp's row boundaries in the padded list of chunk ch
@@ -244,49 +290,6 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         }
       }
       cp_async_commit();
-    };
-    auto fill = [&](int c) {  // this warp's 16 B rows of chunk c -> its TMEM lane quarter
-      ctt_mbar_wait(ctt_smem_u32(&sfull[c % CTT_STAGES]), (uint32_t)((c / CTT_STAGES) & 1));
-      constexpr int kRows = CTT_CHUNK / 4;
-      const float* src = smem + (c % CTT_STAGES) * CTT_STAGE_FLOATS + (kRows * part) * CTT_COLS + lane * 4;
-      const uint32_t dst = tq + (uint32_t)((c & 1) * 4 * CTT_CHUNK + 4 * kRows * part);
-#pragma unroll 8
-      for (int j = 0; j < kRows; ++j) {  // (unrolled: loads run ahead of the TMEM stores)
-        const float4 v = *reinterpret_cast<const float4*>(src + j * CTT_COLS);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + 4 * j),
-                     "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
-                     "r"(__float_as_uint(v.w))
-                     : "memory");
-      }
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[c % CTT_STAGES])) : "memory");
-    };
-    // the same copy split in CTT_RPW / 2 phases of 4 rows, interleaved with the group work of
-    // the current chunk: a phase's LDS.128 are issued before two rows' groups and its tcgen05.st
-    // after them, so the shared-memory latency of the copy hides behind the FMAs
-    constexpr int kFillRows = CTT_CHUNK / 4, kPhases = CTT_RPW / 2, kPhaseRows = kFillRows / kPhases;
-    float4 fv[kPhaseRows];
-    auto fill_load = [&](int c, int ph) {
-      const float* src = smem + (c % CTT_STAGES) * CTT_STAGE_FLOATS + (kFillRows * part + kPhaseRows * ph) * CTT_COLS +
-                         lane * 4;
-#pragma unroll
-      for (int j = 0; j < kPhaseRows; ++j) fv[j] = *reinterpret_cast<const float4*>(src + j * CTT_COLS);
-    };
-    auto fill_store = [&](int c, int ph) {
-      const uint32_t dst = tq + (uint32_t)((c & 1) * 4 * CTT_CHUNK + 4 * (kFillRows * part + kPhaseRows * ph));
-#pragma unroll
-      for (int j = 0; j < kPhaseRows; ++j)
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst + 4 * j),
-                     "r"(__float_as_uint(fv[j].x)), "r"(__float_as_uint(fv[j].y)), "r"(__float_as_uint(fv[j].z)),
-                     "r"(__float_as_uint(fv[j].w))
-                     : "memory");
-    };
-    auto quarter_sync = [&]() {
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
-      asm volatile("tcgen05.fence::after_thread_sync;");
     };
 
     float acc[CTT_RPW][4];
@@ -325,21 +328,11 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
     int meta = load_meta(0);
     int meta_next = load_meta(1);
     stage_list(0, meta);
-    if (n_chunks > 0) fill(0);
-    quarter_sync();
     for (int ch = 0; ch < n_chunks; ++ch) {
       const int meta_after = load_meta(ch + 2);
       stage_list(ch + 1, meta_next);
       cp_async_wait<1>();  // chunk ch's list has landed (ch + 1's may be in flight)
       __syncwarp();
-      const bool next = ch + 1 < n_chunks;
-      if (next) ctt_mbar_wait(ctt_smem_u32(&sfull[(ch + 1) % CTT_STAGES]), (uint32_t)(((ch + 1) / CTT_STAGES) & 1));
-      auto fill_step = [&](int r) {  // before rows r = 0, 2, 4, 6 of chunk ch: one phase of chunk ch + 1
-        if (next && r % 2 == 0) {
-          if (r > 0) fill_store(ch + 1, r / 2 - 1);
-          fill_load(ch + 1, r / 2);
-        }
-      };
       const int e0 = __shfl_sync(0xffffffffu, meta, 0);
       const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
       STC_CHECK(total >= 0 && total % CTT_PAD == 0, "COLTILE chunk list length");
@@ -350,24 +343,24 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
 #pragma unroll
         for (int r = 0; r < CTT_RPW; ++r) {
           const int nr = __shfl_sync(0xffffffffu, ngrp, r);
-          fill_step(r);
           STC_CHECK(nr >= 0 && nr * CTT_PAD <= total, "COLTILE row list outside the chunk list");
 #pragma unroll kGroupUnroll
           for (int g = 0; g < nr; ++g, gp += 2) group(acc[r], gp[0], gp[1]);
         }
       };
+      // chunk ch is in buffer ch & 1 of this quarter once the quarter's fill warp has stored it
+      ctt_mbar_wait(ctt_smem_u32(&tfull[2 * quarter + (ch & 1)]), (uint32_t)((ch / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (total <= CTT_ECAP)
         rows(reinterpret_cast<const int4*>(mylists + (ch & 1) * CTT_ECAP));  // LDS
       else
         rows(reinterpret_cast<const int4*>(ent + e0));                       // LDG
-      if (next) {
-        fill_store(ch + 1, kPhases - 1);
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&sempty[(ch + 1) % CTT_STAGES]))
-                       : "memory");
-      }
-      quarter_sync();  // chunk ch fully read, chunk ch + 1 fully written
+      // every load of this chunk has completed (each group waits): hand the buffer back
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ctt_smem_u32(&tfree[2 * quarter + (ch & 1)]))
+                     : "memory");
       meta = meta_next;
       meta_next = meta_after;
     }
