@@ -87,7 +87,7 @@ int stc_merge_interleave(int m, long long nnz, const int* rowptr, const int* col
 int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int kind);
 
 /* Plan of the COLTILE variant (B operand staged in Tensor Memory): A re-encoded
- * per (128-row block, 64-column chunk, row) as packed {Tensor Memory address
+ * per (224-row block, 63-column chunk, row) as packed {Tensor Memory address
  * of the operand row, value} entries, each row padded with zero-weight
  * entries to a multiple of 4 (the layout is private to the kernel).
  * The plan CARRIES A's VALUES (the prepared form of A, like a cuSPARSE SpMM

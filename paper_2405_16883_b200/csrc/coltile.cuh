@@ -1,6 +1,6 @@
 // K3: column-tiled CSR SpMM with the dense operand staged in Tensor Memory (sm_100a).
 //
-// C[r, c0:c0+128] = sum_p val[p] * B[col[p], c0:c0+128] for a block of 128 rows.
+// C[r, c0:c0+128] = sum_p val[p] * B[col[p], c0:c0+128] for a block of 224 rows (28 consumer warps x 8 rows).
 //
 // Operand path:  global --one tiled TMA copy per chunk (tensor map)--> SMEM stage (63 B rows x
 //                512 B + one all-zero row that padding entries point at)
@@ -13,16 +13,17 @@
 // No MMA is issued — tensor cores stay off this path (north star); TMEM serves as
 // a wide operand buffer for CUDA-core FMAs.
 //
-// Entry path: the plan (`stc_coltile_plan`) re-encodes A per (128-row block,
-// 64-column chunk, row) as packed entries {TMEM address of B[col] for the row's warp and
-// the chunk's buffer, value bits}, each row padded with zero-weight entries to a multiple
-// of 4 — the inner loop adds nothing to the addresses it loads. A warp's list for a chunk
-// is contiguous: it is copied into SMEM with cp.async one chunk ahead, and
-// the inner loop is two LDS.128 (4 entries) + 4 tcgen05.ld + one wait::ld + 16 FFMA.
+// Entry path: the plan (`stc_coltile_plan`) re-encodes A per (224-row block,
+// 63-column chunk, row) as packed entries {TMEM address of B[col] for the row's warp and
+// the chunk's buffer, value bits}, each row padded to an even count with a zero-weight entry
+// that points at the chunk's all-zero slot — the inner loop adds nothing to the addresses it
+// loads and has no masked case. A warp's list for a chunk is contiguous: it is copied into
+// SMEM with cp.async one chunk ahead, and the inner loop is two LDS.128 (4 entries) + 4
+// tcgen05.ld + one wait::ld + 8 FFMA2 (a row's odd pair: half of that).
 // The plan carries the VALUES of A (it is the prepared form of the matrix, like a
 // cuSPARSE SpMM preprocess): rebuild it when the values change.
 //
-// Pipeline (1 CTA/SM, 640 threads, TMEM = 2 buffers x 256 columns, all hand-offs by mbarrier):
+// Pipeline (1 CTA/SM, 1024 threads, TMEM = 2 buffers x 256 columns, all hand-offs by mbarrier):
 //   fill warp q    : (q = 0 also issues the TMA copies, two chunks ahead: one
 //   (4 warps)        cp.async.bulk.tensor.2d, 63 x 128 box, zero fill past n / k, into stage c % 3
 //                    once all four fill warps have left chunk c - 1's stage -- `sempty`; an operand
@@ -31,7 +32,7 @@
 //                    the tiled copy.) Waits for the stage (`sfull`, transaction bytes) and for its
 //                    quarter's buffer c & 1 to be read (`tfree[q]`), copies the 64 slots into the
 //                    quarter (LDS.128 -> tcgen05.st), then arrives on `tfull[q]` and `sempty`.
-//   16 consumer    : wait `tfull[quarter]`, consume chunk c from TMEM, arrive on `tfree[quarter]`.
+//   28 consumer    : wait `tfull[quarter]`, consume chunk c from TMEM, arrive on `tfree[quarter]`.
 //   warps            (Round 2: the consumers used to copy the chunks themselves, interleaved with
 //                    their group loop, and met at a named barrier per quarter: 3.84 -> 3.61 ms.
 //                    tcgen05.cp.32x128b.warpx4 as the copy engine was measured too: ~40 cycles per
@@ -47,19 +48,26 @@
 namespace stc {
 
 #ifndef CTT_GROUP_UNROLL
-#define CTT_GROUP_UNROLL 2
+#define CTT_GROUP_UNROLL 1
 #endif
 constexpr int kGroupUnroll = CTT_GROUP_UNROLL;    // groups per unrolled body of a row's loop
-constexpr int CTT_ROWS = 128;
+#ifndef CTT_CONSUMER_WARPS
+#define CTT_CONSUMER_WARPS 28
+#endif
+// Consumer warps (a multiple of 4: warp % 4 = TMEM lane quarter). The group loop is a chain of
+// dependent latencies (list LDS -> R2UR -> tcgen05.ld -> wait::ld -> FFMA2), so it is the number of
+// resident warps that sets the rate: cfg3 3.61 ms at 16 warps (96 registers), 3.34 at 20, 3.10 at 24,
+// 2.98 at 28 (64 registers, 224-row blocks: 2368 CTAs = 16 full waves of 148).
+constexpr int CTT_WARPS = CTT_CONSUMER_WARPS;
+constexpr int CTT_RPW = 8;                        // rows per consumer warp
+constexpr int CTT_ROWS = CTT_WARPS * CTT_RPW;
 constexpr int CTT_COLS = 128;
 constexpr int CTT_CHUNK = 64;                     // operand slots per chunk in SMEM / TMEM
 constexpr int CTT_BROWS = CTT_CHUNK - 1;          // B rows per chunk; the last slot is an all-zero row
-constexpr int CTT_WARPS = 16;                      // consumer warps
 constexpr int CTT_FILL_WARPS = 4;                  // one per TMEM lane quarter: SMEM stage -> TMEM
-constexpr int CTT_THREADS = (CTT_WARPS + CTT_FILL_WARPS) * 32;  // 640: 96 registers per thread still fit
+constexpr int CTT_THREADS = (CTT_WARPS + CTT_FILL_WARPS) * 32;  // 1024 threads, 64 registers each
 constexpr int CTT_STAGES = 3;
-constexpr int CTT_RPW = CTT_ROWS / CTT_WARPS;     // rows per consumer warp
-constexpr int CTT_PAD = 4;                        // row segments padded to this many entries
+constexpr int CTT_PAD = 2;                        // row segments padded to this many entries (one 16-byte list element)
 constexpr int CTT_ECAP = 128;                     // staged entries per warp and chunk
 constexpr int CTT_ZERO_SLOT = 4 * CTT_BROWS;      // TMEM column of the zero row inside a chunk's buffer
 constexpr size_t CTT_STAGE_FLOATS = (size_t)CTT_CHUNK * CTT_COLS;
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
     float acc[CTT_RPW][4];
 #pragma unroll
     for (int r = 0; r < CTT_RPW; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
-    // 4 entries -> 4 tcgen05.ld, one wait, 8 packed FMAs (padding entries: weight 0 on the zero slot)
+    // 4 entries -> 4 tcgen05.ld, one wait, 8 packed FMAs (a padding entry: weight 0 on the zero slot)
     auto group = [&](float (&a)[4], int4 e01, int4 e23) {
       uint32_t x[4][4];
       const int taddr[4] = {e01.x, e01.z, e23.x, e23.z};  // absolute TMEM addresses (plan)
@@ -324,6 +332,32 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
         fma2(a[2], a[3], w[u], __uint_as_float(x[u][2]), __uint_as_float(x[u][3]));
       }
     };
+    // a row's last pair when its padded count is not a multiple of 4 (rows are padded to pairs:
+    // 0.5 padding entries per row and chunk on average instead of 1.5 with groups of 4 only)
+    auto pair = [&](float (&a)[4], int4 e01) {
+      uint32_t x[2][4];
+      const int taddr[2] = {e01.x, e01.z};
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        STC_CHECK((uint32_t)taddr[u] >> 16 == 32u * quarter && (taddr[u] & 0xffff) < 512,
+                  "COLTILE entry outside the warp's TMEM lane quarter");
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x[u][0]), "=r"(x[u][1]), "=r"(x[u][2]), "=r"(x[u][3])
+                     : "r"(taddr[u]));
+      asm volatile("tcgen05.wait::ld.sync.aligned;"
+                   : "+r"(x[0][0]), "+r"(x[0][1]), "+r"(x[0][2]), "+r"(x[0][3]), "+r"(x[1][0]), "+r"(x[1][1]),
+                     "+r"(x[1][2]), "+r"(x[1][3])
+                   :
+                   : "memory");
+      const float w[2] = {__int_as_float(e01.y), __int_as_float(e01.w)};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        fma2(a[0], a[1], w[u], __uint_as_float(x[u][0]), __uint_as_float(x[u][1]));
+        fma2(a[2], a[3], w[u], __uint_as_float(x[u][2]), __uint_as_float(x[u][3]));
+      }
+    };
 
     int meta = load_meta(0);
     int meta_next = load_meta(1);
@@ -336,16 +370,17 @@ __global__ void __launch_bounds__(CTT_THREADS, 1)
       const int e0 = __shfl_sync(0xffffffffu, meta, 0);
       const int total = __shfl_sync(0xffffffffu, meta, CTT_RPW) - e0;
       STC_CHECK(total >= 0 && total % CTT_PAD == 0, "COLTILE chunk list length");
-      // lane r: groups of row r in this chunk; the rows' groups are contiguous in the list, so one
+      // lane r: pairs of row r in this chunk; the rows' pairs are contiguous in the list, so one
       // pointer walks it (chunks denser than the staged list read it straight from global memory)
-      const int ngrp = (__shfl_down_sync(0xffffffffu, meta, 1) - meta) / CTT_PAD;
-      auto rows = [&](const int4* gp) {
+      const int npair = (__shfl_down_sync(0xffffffffu, meta, 1) - meta) / CTT_PAD;
+      auto rows = [&](const int4* gp) {  // one int4 = one pair of entries
 #pragma unroll
         for (int r = 0; r < CTT_RPW; ++r) {
-          const int nr = __shfl_sync(0xffffffffu, ngrp, r);
+          const int nr = __shfl_sync(0xffffffffu, npair, r);
           STC_CHECK(nr >= 0 && nr * CTT_PAD <= total, "COLTILE row list outside the chunk list");
 #pragma unroll kGroupUnroll
-          for (int g = 0; g < nr; ++g, gp += 2) group(acc[r], gp[0], gp[1]);
+          for (int g = 0; g < (nr >> 1); ++g, gp += 2) group(acc[r], gp[0], gp[1]);
+          if (nr & 1) pair(acc[r], *gp++);
         }
       };
       // chunk ch is in buffer ch & 1 of this quarter once the quarter's fill warp has stored it

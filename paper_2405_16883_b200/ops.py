@@ -75,8 +75,8 @@ def choose_variant(stats: RowStats, k: int, aligned: bool = True, n_cols: int | 
     tiles {k} (scheduler.py / tiling.py); on the device the same plan splits
     into three variants by the shape of the data.
 
-    COLTILE reads every B row of a column slab once per 128-row block, i.e. B's bytes
-    m / 128 times, where the gather variants read nnz rows: it is chosen only for wide
+    COLTILE reads every B row of a column slab once per 224-row block, i.e. B's bytes
+    m / 224 times, where the gather variants read nnz rows: it is chosen only for wide
     dense operands when A is dense enough (nnz >= m * n / 128) and its plan fits int32."""
     if k >= COLTILE_MIN_K and aligned and coltile_fits(stats, n_cols):
         return "coltile"
