@@ -46,27 +46,17 @@ struct MttkrpItemsOp {
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
     STC_CHECK(!it.flag || (unsigned long long)(it.offb + lane_off) + VEC <= limitb, "MTTKRP gather outside B");
     STC_CHECK((unsigned long long)(it.offc + lane_off) + VEC <= limitc, "MTTKRP gather outside C");
-#ifdef STC_MTTKRP_COLDHOT
-    // experiment: rows the plan marked cold (flag bits 1 / 2) are gathered without an L1 allocation,
-    // so the in-flight misses do not push the hot factor rows out of the L1
-    if (it.flag & 1) {
-      if (it.flag & 4) pre.b.load_stream(B + (it.offb + lane_off));
-      else pre.b.load_gather(B + (it.offb + lane_off));
-    }
-    if (it.flag & 2) pre.c.load_stream(C + (it.offc + lane_off));
-    else pre.c.load_gather(C + (it.offc + lane_off));
-#else
     if (it.flag) pre.b.load_gather(B + (it.offb + lane_off));
     pre.c.load_gather(C + (it.offc + lane_off));
-#endif
   }
   STC_DEVICE static void init(State& st) { st.b.zero(); }
   STC_DEVICE void accumulate(Frag<VEC>& acc, State& st, const Pre& pre, const Item& it) const {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) st.b.v[e] = (it.flag & 1) ? pre.b.v[e] : st.b.v[e];
-#ifdef STC_MTTKRP_F2
+#ifndef STC_MTTKRP_NO_F2
     if constexpr (VEC % 2 == 0) {
-      // packed halves: each is exactly mul.rn / fma.rn, so the sums do not change
+      // packed halves (FMUL2 / FFMA2): each is exactly mul.rn / fma.rn, so the sums do not change;
+      // half the issue slots of the product chain (cfg5 114.7 -> 112.7 us)
 #pragma unroll
       for (int e = 0; e < VEC; e += 2) {
         float t0, t1;
@@ -93,12 +83,7 @@ __global__ void mttkrp_items_kernel(long long nnz, const int* __restrict__ jc, c
        p += (long long)gridDim.x * blockDim.x) {
     const int j = jc[p];
     const bool start = p == 0 || jc[p - 1] != j;
-    int flag = start ? 1 : 0;
-#ifdef STC_MTTKRP_COLDHOT
-    if (kc[p] >= STC_MTTKRP_COLDHOT) flag |= 2;
-    if (j >= STC_MTTKRP_COLDHOT) flag |= 4;
-#endif
-    items[p] = Item{(unsigned)((long long)j * ldb), (unsigned)((long long)kc[p] * ldcf), val[p], flag};
+    items[p] = Item{(unsigned)((long long)j * ldb), (unsigned)((long long)kc[p] * ldcf), val[p], start ? 1 : 0};
   }
 }
 

@@ -159,11 +159,6 @@ struct Frag<4> {
     float4 t = *reinterpret_cast<const float4*>(p);
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
   }
-  // read-only gather that leaves no line in the L1
-  STC_DEVICE void load_stream(const float* p) {
-    float4 t = ld_stream4(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  }
   // L2-coherent read of data published by another CTA in the same launch
   STC_DEVICE void load_l2(const float* p) {
     float4 t = __ldcg(reinterpret_cast<const float4*>(p));
@@ -180,7 +175,6 @@ struct Frag<1> {
   float v[1];
   STC_DEVICE void zero() { v[0] = 0.f; }
   STC_DEVICE void load_gather(const float* p) { v[0] = ld_gather1(p); }
-  STC_DEVICE void load_stream(const float* p) { v[0] = ld_stream(p); }
   STC_DEVICE void load_plain(const float* p) { v[0] = *p; }
   STC_DEVICE void load_l2(const float* p) { v[0] = __ldcg(p); }
   STC_DEVICE void store_stream(float* p) const { st_stream1(p, v[0]); }
