@@ -527,3 +527,30 @@ def test_merge_carries_bitwise_stable_over_many_launches(ipg):
     want = native.spmm_csr(rp, ci, v, B.cpu().numpy().astype(np.float64), relu=True)
     bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B.cpu().numpy().astype(np.float64)))
     assert parity_gate(first.cpu().numpy(), want, bound, TOL)[0]
+
+
+# ---- COLTILE stage / TMEM-buffer hand-offs under repetition -----------------------------------
+
+def test_coltile_pipeline_bitwise_stable_over_many_launches():
+    """COLTILE hands B chunks from the TMA stage ring to the four fill warps and on to the 28
+    consumer warps through mbarriers (stage landed / stage copied, TMEM buffer written / read, per
+    lane quarter). A missed wait shows up as a stale or half-written chunk: 40 chunks per CTA
+    (n = 2500), unequal work per warp (row lengths 0..300), two column tiles with a ragged edge
+    (k = 132), 100 back-to-back launches -- all outputs must be bit-identical and equal to the
+    oracle, with an addend + ReLU epilogue as well."""
+    rng = np.random.default_rng(77)
+    m, n, k = 500, 2500, 132
+    lens = np.where(np.arange(m) % 7 == 0, 300, rng.integers(0, 40, m))
+    rp, ci, v = make_csr(rng, m, n, lens)
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    D = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    R, C, V = dev(rp, ci, v)
+    Bt, Dt = torch.from_numpy(B).cuda(), torch.from_numpy(D).cuda()
+    plan = ops.coltile_plan(R, C, n, V)
+    first = ops.spmm_csr(R, C, V, Bt, addend=Dt, relu=True, variant="coltile", partition=plan)
+    outs = [ops.spmm_csr(R, C, V, Bt, addend=Dt, relu=True, variant="coltile", partition=plan) for _ in range(100)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(first, o) for o in outs)
+    want = native.spmm_csr(rp, ci, v, B, addend=D, relu=True)
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B), addend=np.abs(D))
+    assert parity_gate(first.cpu().numpy(), want, bound, TOL)[0]
