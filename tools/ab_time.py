@@ -18,6 +18,7 @@ flush = torch.empty(128 * 1024 * 1024, device="cuda")
 ts = []
 for _ in range(int(os.environ.get("REPS", "30"))):
     flush.zero_()
+    flush.sum()  # clean L2 (bench.py flush_l2)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     fn()

@@ -46,6 +46,7 @@ def gpu_time(fn, reps=20):
     torch.cuda.synchronize()
     for _ in range(reps):
         FLUSH.zero_()
+        FLUSH.sum()  # read-back: the L2 is left with clean lines (bench.py flush_l2)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
