@@ -88,8 +88,14 @@ int stc_merge_plan_items_per_group(int m, long long nnz, int k, int batch, int k
 
 /* Plan of the COLTILE variant (B operand staged in Tensor Memory): A re-encoded
  * per (224-row block, 63-column chunk, row) as packed {Tensor Memory address
- * of the operand row, value} entries, each row padded with zero-weight
- * entries to a multiple of 4 (the layout is private to the kernel).
+ * of the operand row, value} entries, each row padded to an even count with a
+ * zero-weight entry on an all-zero operand slot (the layout is private to the
+ * kernel). The kernel stages B through a tiled TMA copy: it builds a tensor
+ * map of B per launch (B and its pitch must be 16-byte aligned, as for every
+ * vectorised variant); the encoder is a driver entry point fetched through the
+ * runtime, and when it is unavailable -- or STC_COLTILE_ROW_COPIES=1 is set in
+ * the environment, a test hook -- B is staged by one bulk copy per row instead
+ * (same results, slower).
  * The plan CARRIES A's VALUES (the prepared form of A, like a cuSPARSE SpMM
  * preprocess): rebuild it whenever the values change. stc_coltile_plan_ints
  * gives its size in int32 (-1 if unsupported); pass it as the `partition` of a
