@@ -229,6 +229,21 @@ class ColtilePlan:
 
     plan: torch.Tensor
     nnz: int
+    m: int = -1               # rows / operand rows of the structure the plan was built for
+    n: int = -1
+    source: tuple | None = None   # (data_ptr, _version) of the colidx / vals the plan encodes
+
+    def check(self, m: int, n: int, nnz: int, colidx: torch.Tensor, vals: torch.Tensor) -> None:
+        """Raise if this plan encodes another matrix: the kernel indexes the plan with the
+        call's m and n, and computes with the values stored in the plan."""
+        if self.m >= 0 and (self.m, self.n, self.nnz) != (m, n, nnz):
+            raise ValueError(f"COLTILE plan built for m={self.m}, n={self.n}, nnz={self.nnz}; "
+                             f"matrix has m={m}, n={n}, nnz={nnz}")
+        if self.nnz != nnz:
+            raise ValueError(f"COLTILE plan built for nnz={self.nnz}, matrix has {nnz}")
+        if self.source is not None and self.source != _buffer_id(colidx, vals):
+            raise ValueError("COLTILE plan carries the entries of another colidx/vals (or of values "
+                             "modified since): rebuild it with coltile_plan(rowptr, colidx, n, vals)")
 
 
 @on_operand_device
@@ -242,7 +257,7 @@ def coltile_plan(rowptr: torch.Tensor, colidx: torch.Tensor, n_cols: int, vals: 
     plan = torch.empty(max(ints, 1), dtype=torch.int32, device=rowptr.device)
     check(lib().stc_coltile_plan(m, n_cols, nnz, ptr(_i32(rowptr)), ptr(_i32(colidx)), ptr(_f32(vals)), ptr(plan),
                                  ints, stream_handle()), "stc_coltile_plan")
-    return ColtilePlan(plan, nnz)
+    return ColtilePlan(plan, nnz, m, int(n_cols), _buffer_id(colidx, vals))
 
 
 def spmm_workspace(m: int, nnz: int, k: int, variant: str, items_per_group: int, batch: int,
@@ -301,8 +316,7 @@ def spmm_csr(rowptr: torch.Tensor, colidx: torch.Tensor, vals: torch.Tensor, B: 
             workspace = partition.workspace(k, 1, B.device)
     elif variant == "coltile":
         partition = partition or coltile_plan(rowptr, colidx, n, vals)
-        if partition.nnz != nnz:
-            raise ValueError(f"COLTILE plan built for nnz={partition.nnz}, matrix has {nnz}")
+        partition.check(m, n, nnz, colidx, vals)
         plan_ptr = ptr(partition.plan)
     ws_bytes = 0 if workspace is None else workspace.numel() * 4
     rc = lib().stc_spmm_csr_f32(

@@ -554,3 +554,22 @@ def test_coltile_pipeline_bitwise_stable_over_many_launches():
     want = native.spmm_csr(rp, ci, v, B, addend=D, relu=True)
     bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B), addend=np.abs(D))
     assert parity_gate(first.cpu().numpy(), want, bound, TOL)[0]
+
+
+def test_coltile_plan_rejects_another_matrix():
+    """A COLTILE plan encodes one matrix (structure and values): using it with another m / n /
+    nnz, other buffers, or values modified in place must raise instead of computing with stale
+    entries or indexing the plan out of range."""
+    rng = np.random.default_rng(5)
+    rp, ci, v = make_csr(rng, 300, 200, rng.integers(0, 30, 300))
+    R, C, V = dev(rp, ci, v)
+    B = torch.randn(200, 128, device="cuda")
+    plan = ops.coltile_plan(R, C, 200, V)
+    ops.spmm_csr(R, C, V, B, variant="coltile", partition=plan)
+    with pytest.raises(ValueError):
+        ops.spmm_csr(R, C, V.clone(), B, variant="coltile", partition=plan)      # other value buffer
+    with pytest.raises(ValueError):
+        ops.spmm_csr(R, C, V, torch.randn(264, 128, device="cuda"), variant="coltile", partition=plan)  # other n
+    V.mul_(2.0)                                                                   # values changed in place
+    with pytest.raises(ValueError):
+        ops.spmm_csr(R, C, V, B, variant="coltile", partition=plan)
