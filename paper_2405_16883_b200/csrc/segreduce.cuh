@@ -648,7 +648,9 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_kernel(SegOut o, Me
   if (lane == 0 && g < (1 << 16) && blockIdx.y == 0 && blockIdx.z == 0) {
     g_dbg[g][0] = t_start;
     g_dbg[g][1] = dbg_timer();
-    g_dbg[g][2] = (unsigned long long)n_rows;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_dbg[g][2] = (unsigned long long)n_rows | ((unsigned long long)smid << 32);
     g_dbg[g][3] = ((unsigned long long)n_nnz << 32) | (unsigned)(threadIdx.x / 32 + (blockIdx.x << 8));
   }
 #endif

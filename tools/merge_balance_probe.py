@@ -22,7 +22,7 @@ R, C, V = (torch.from_numpy(A.rowptr).int().cuda(), torch.from_numpy(A.colidx).i
            torch.from_numpy(A.vals).cuda())
 Z = torch.from_numpy(X).cuda() @ torch.from_numpy(W1).cuda()
 out = torch.empty_like(Z)
-part = ops.merge_partition(R, A.nnz, k=128)
+part = ops.merge_partition(R, A.nnz, k=128, colidx=C, vals=V)  # the shipped plan: long rows interleaved
 ws = ops.spmm_workspace(A.shape[0], A.nnz, 128, "merge", part.items_per_group, 1, "cuda")
 FL = torch.empty(128 * 1024 * 1024, device="cuda")
 for _ in range(5):
@@ -40,7 +40,8 @@ d = buf[:G]
 t0, t1 = d[:, 0].astype(np.int64), d[:, 1].astype(np.int64)
 base = t0.min()
 start, end = (t0 - base) / 1e3, (t1 - base) / 1e3
-rows = d[:, 2].astype(np.int64)
+rows = (d[:, 2] & np.uint64(0xffffffff)).astype(np.int64)
+smid = (d[:, 2] >> np.uint64(32)).astype(np.int64)
 nnz = (d[:, 3] >> np.uint64(32)).astype(np.int64)
 dur = end - start
 print(f"groups {G} ipg {part.items_per_group}; kernel span {end.max():.1f} us")
@@ -64,3 +65,23 @@ fast = np.argsort(end)[:5]
 print("fastest groups:")
 for gi in fast:
     print(f"  {gi:5d} {cta[gi]:4d} {rows[gi]:4d} {nnz[gi]:4d} {start[gi]:6.1f} {end[gi]:6.1f}")
+
+# ---- what explains the spread: cold gathers per group, or the SM a group ran on? ----
+st = part.starts.cpu().numpy().reshape(-1, 2)
+ci = (part.colidx if part.colidx is not None else C).cpu().numpy()
+p0, p1 = st[:G, 1], st[1:G + 1, 1]
+for thr in (2000, 20000, 60000):
+    cold_pref = np.concatenate([[0], np.cumsum(ci >= thr)])
+    cold = cold_pref[p1] - cold_pref[p0]
+    X_ = np.stack([np.ones(G), rows, cold], 1)
+    coef, *_ = np.linalg.lstsq(X_, end, rcond=None)
+    res = end - X_ @ coef
+    print(f"cold = col >= {thr}: corr(finish, cold) {np.corrcoef(end, cold)[0, 1]:.3f}; finish ~ {coef[0]:.1f} + "
+          f"{coef[1]:.4f} rows + {coef[2]:.4f} cold; residual sd {res.std():.2f} us (finish sd {end.std():.2f})")
+sm_mean = np.zeros(smid.max() + 1)
+sm_cnt = np.zeros(smid.max() + 1)
+np.add.at(sm_mean, smid, end)
+np.add.at(sm_cnt, smid, 1)
+sm_mean = sm_mean[sm_cnt > 0] / sm_cnt[sm_cnt > 0]
+print(f"per-SM mean finish: min {sm_mean.min():.1f} p50 {np.median(sm_mean):.1f} max {sm_mean.max():.1f} us; "
+      f"sd between SMs {sm_mean.std():.2f}, sd within SMs {np.sqrt(max(end.var() - sm_mean.var(), 0)):.2f}")
