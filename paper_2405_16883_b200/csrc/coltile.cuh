@@ -5,7 +5,7 @@
 // Operand path:  global --one tiled TMA copy per chunk (tensor map)--> SMEM stage (63 B rows x
 //                512 B + one all-zero row that padding entries point at)
 //                --LDS.128 + tcgen05.st (one fill warp per TMEM lane quarter)--> TMEM
-//                --tcgen05.ld.32x32b.x4 (16 consumer warps)--> registers (lane l: B[j, c0+4l .. c0+4l+3])
+//                --tcgen05.ld.32x32b.x4 (28 consumer warps)--> registers (lane l: B[j, c0+4l .. c0+4l+3])
 // Each staged row is reused by every row of the block holding that column (~12.8
 // at 10 % density). Reading the operand from TMEM takes it off the SMEM crossbar,
 // which caps an SMEM-staged kernel near a quarter of the FP32 peak (the previous
@@ -57,7 +57,7 @@ constexpr int kGroupUnroll = CTT_GROUP_UNROLL;    // groups per unrolled body of
 // Consumer warps (a multiple of 4: warp % 4 = TMEM lane quarter). The group loop is a chain of
 // dependent latencies (list LDS -> R2UR -> tcgen05.ld -> wait::ld -> FFMA2), so it is the number of
 // resident warps that sets the rate: cfg3 3.61 ms at 16 warps (96 registers), 3.34 at 20, 3.10 at 24,
-// 2.98 at 28 (64 registers, 224-row blocks: 2368 CTAs = 16 full waves of 148).
+// 2.93 at 28 (64 registers, 224-row blocks: 2368 CTAs = 16 full waves of 148).
 constexpr int CTT_WARPS = CTT_CONSUMER_WARPS;
 constexpr int CTT_RPW = 8;                        // rows per consumer warp
 constexpr int CTT_ROWS = CTT_WARPS * CTT_RPW;
