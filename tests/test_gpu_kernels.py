@@ -573,3 +573,29 @@ def test_coltile_plan_rejects_another_matrix():
     V.mul_(2.0)                                                                   # values changed in place
     with pytest.raises(ValueError):
         ops.spmm_csr(R, C, V, B, variant="coltile", partition=plan)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_coltile_random_shapes(seed):
+    """COLTILE forced on random shapes around its block edges (224-row blocks, 63-row operand
+    chunks, 128-column tiles): ragged last block / chunk / tile, empty rows, rows denser than the
+    staged list, addend and ReLU epilogues -- against the float64 oracle."""
+    rng = np.random.default_rng(9000 + seed)
+    m = int(rng.choice([1, 7, 223, 224, 225, 449, int(rng.integers(1, 700))]))
+    n = int(rng.choice([1, 62, 63, 64, 126, 127, int(rng.integers(1, 400))]))
+    k = 4 * int(rng.choice([1, 31, 32, 33, 64, int(rng.integers(1, 70))]))
+    dens = float(rng.choice([0.0, 0.02, 0.3, 1.0]))
+    lens = rng.binomial(n, dens, m)
+    lens[rng.random(m) < 0.2] = 0
+    rp, ci, v = make_csr(rng, m, n, lens)
+    B = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    D = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    R, C, V = dev(rp, ci, v)
+    relu = bool(seed & 1)
+    use_d = bool(seed & 2)
+    got = ops.spmm_csr(R, C, V, torch.from_numpy(B).cuda(), variant="coltile", relu=relu,
+                       addend=torch.from_numpy(D).cuda() if use_d else None).cpu().numpy()
+    want = native.spmm_csr(rp, ci, v, B, addend=D if use_d else None, relu=relu)
+    bound = native.spmm_csr(rp, ci, np.abs(v), np.abs(B), addend=np.abs(D) if use_d else None)
+    ok, worst = parity_gate(got, want, bound, TOL)
+    assert ok, (m, n, k, dens, worst)
