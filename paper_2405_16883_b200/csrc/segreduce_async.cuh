@@ -255,7 +255,16 @@ __global__ void __launch_bounds__(256, Op::kMinBlocks) merge_async_kernel(SegOut
     }
     const int cw = c * W;
     end_w = cur_end - cw;
-    if (cw + W <= n_nnz) {  // full chunk: W / U ring turns, entry t + U lies in this chunk or the next
+    // Fast path, taken warp-wide: every group of the warp has a full chunk with no row end in it
+    // (most chunks: a group owns ~350 entries and one or two row ends). Straight-line code with no
+    // flush scaffolding, so the operand bases and load descriptors stay in uniform registers.
+    if (__all_sync(0xffffffffu, cw + W <= n_nnz && end_w >= W)) {
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        op.accumulate(acc, fst, ring[t % U], cur[t]);
+        if (col_ok) op.fetch(t + U < W ? cur[t + U] : nxt[t + U - W], ring[t % U]);
+      }
+    } else if (cw + W <= n_nnz) {  // full chunk: W / U ring turns, entry t + U lies in this chunk or the next
       // unrolled F entries at a time (F a multiple of the ring depth, so ring slots stay
       // static): the fully unrolled chunk with its inlined flush paths is ~25 k SASS lines
       // and stalls on instruction fetch (no_instruction 9 % of samples at F = W = 16)
