@@ -17,19 +17,30 @@ int check_common(int m, int n, int d, int heads, const int* rowptr, long long nn
   return STC_OK;
 }
 
+// every gathered row of K (and V) starts below 2^31 elements: the kernels take 32-bit row offsets
+bool narrow_rows(const AttnArgs& a, bool with_v) {
+  return (long long)a.n * a.k_rs < (1LL << 31) && (!with_v || (long long)a.n * a.v_rs < (1LL << 31));
+}
+
 bool dim_ok(int d) { return d == 4 || d == 8 || d == 16 || d == 32 || d == 64 || d == 128; }
 
 template <int G>
 int launch_sddmm(const AttnArgs& a, cudaStream_t st) {
   const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
-  sddmm_kernel<G><<<grid, kThreads, 0, st>>>(a);
+  if (narrow_rows(a, false))
+    sddmm_kernel<G, true><<<grid, kThreads, 0, st>>>(a);
+  else
+    sddmm_kernel<G, false><<<grid, kThreads, 0, st>>>(a);
   return check_launch("sddmm_kernel");
 }
 
 template <int G, bool WS>
 int launch_attn(const AttnArgs& a, cudaStream_t st) {
   const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
-  attention_kernel<G, WS><<<grid, kThreads, 0, st>>>(a);
+  if (narrow_rows(a, true))
+    attention_kernel<G, WS, true><<<grid, kThreads, 0, st>>>(a);
+  else
+    attention_kernel<G, WS, false><<<grid, kThreads, 0, st>>>(a);
   return check_launch("attention_kernel");
 }
 
@@ -39,11 +50,16 @@ int launch_attn_vsmem(const AttnArgs& a, cudaStream_t st) {
   constexpr size_t smem = (size_t)(G / 2) * kThreads * sizeof(float4);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(attention_vsmem_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attention_vsmem_kernel<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attention_vsmem_kernel<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   const dim3 grid((unsigned)ceil_div((long long)a.m * G, kThreads), a.heads);
-  attention_vsmem_kernel<G><<<grid, kThreads, smem, st>>>(a);
+  // 32-bit row offsets when every gathered row of K and V starts below 2^31 elements
+  if (narrow_rows(a, true))
+    attention_vsmem_kernel<G, true><<<grid, kThreads, smem, st>>>(a);
+  else
+    attention_vsmem_kernel<G, false><<<grid, kThreads, smem, st>>>(a);
   return check_launch("attention_vsmem_kernel");
 }
 

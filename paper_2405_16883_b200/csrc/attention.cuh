@@ -88,7 +88,7 @@ STC_DEVICE float group_sum(float x, unsigned mask) {
 }
 
 // SDDMM: S[h, p] = scale * mask[p] * dot(Q[h,i,:], K[h,col[p],:])
-template <int G>
+template <int G, bool NARROW>
 __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
   const int lane = threadIdx.x % G;
   const unsigned mask = subwarp_mask<G>();
@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
   if (row >= a.m) return;
   const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
   const float* Kh = a.K + h * a.k_hs + lane * 4;
+  const unsigned krs = (unsigned)a.k_rs;
+  if constexpr (NARROW) asm volatile("" : "+l"(Kh));  // see attention_body
   float* out = a.S + h * a.nnz;
   const int start = a.rowptr[row], end = a.rowptr[row + 1];
   for (int base = start; base < end; base += G) {
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(256) sddmm_kernel(AttnArgs a) {
       const int c = __shfl_sync(mask, my_col, t, G);
       float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
       STC_CHECK(t >= n || (c >= 0 && c < a.n), "SDDMM column outside K");
-      if (t < n) kv = ld_gather4(Kh + (long long)c * a.k_rs);
+      if (t < n) kv = ld_gather4(NARROW ? Kh + (unsigned)c * krs : Kh + (long long)c * a.k_rs);
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
     const float s = transpose_reduce<G>(part, lane, mask);
@@ -149,7 +151,10 @@ __global__ void __launch_bounds__(256) segsoftmax_kernel(int m, long long nnz, c
 #ifndef STC_ATTN_VSMEM_MINB
 #define STC_ATTN_VSMEM_MINB 4
 #endif
-template <int G, bool WRITE_S, bool VSMEM>
+// NARROW: n * row stride of K and V below 2^31 elements (checked by the launcher), so a gathered row's
+// offset is one 32-bit multiply instead of a 64 x 64-bit product per gather -- integer address
+// arithmetic was 45 % of the remainder pass's instructions (IMAD 24 %, LEA 8 %, MOV 8 %, LDC 4 %).
+template <int G, bool WRITE_S, bool VSMEM, bool NARROW = false>
 STC_DEVICE void attention_body(const AttnArgs& a) {
   constexpr int B = G >= 16 ? G / 2 : G;
   extern __shared__ __align__(16) float4 vstage[];  // VSMEM: [B][256] float4, slot [t][thread]
@@ -161,6 +166,15 @@ STC_DEVICE void attention_body(const AttnArgs& a) {
   const float4 q = *reinterpret_cast<const float4*>(a.Q + h * a.q_hs + (long long)row * a.q_rs + lane * 4);
   const float* Kh = a.K + h * a.k_hs + lane * 4;
   const float* Vh = a.V + h * a.v_hs + lane * 4;
+  const unsigned krs = (unsigned)a.k_rs, vrs = (unsigned)a.v_rs;
+  if constexpr (NARROW) {
+    // keep the two row bases as opaque 64-bit registers: otherwise they are re-derived from the
+    // kernel parameters for every gather (LDC + 64-bit add chain, 5-6 instructions per address)
+    asm volatile("" : "+l"(Kh));
+    asm volatile("" : "+l"(Vh));
+  }
+  auto krow = [&](int c) { return NARROW ? Kh + (unsigned)c * krs : Kh + (long long)c * a.k_rs; };
+  auto vrow = [&](int c) { return NARROW ? Vh + (unsigned)c * vrs : Vh + (long long)c * a.v_rs; };
   const int start = a.rowptr[row], end = a.rowptr[row + 1];
   float run_max = -INFINITY, run_sum = 0.f;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -183,10 +197,10 @@ STC_DEVICE void attention_body(const AttnArgs& a) {
       if constexpr (!VSMEM) vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
       STC_CHECK(t >= n || (c >= 0 && c < a.n), "attention column outside K/V");
       if constexpr (VSMEM)  // zero-filled past the row's end
-        cp_async16(&vstage[t * 256 + threadIdx.x], Vh + (long long)(t < n ? c : 0) * a.v_rs, t < n);
+        cp_async16(&vstage[t * 256 + threadIdx.x], vrow(t < n ? c : 0), t < n);
       if (t < n) {
-        kv = ld_gather4(Kh + (long long)c * a.k_rs);
-        if constexpr (!VSMEM) vv[t] = ld_gather4(Vh + (long long)c * a.v_rs);
+        kv = ld_gather4(krow(c));
+        if constexpr (!VSMEM) vv[t] = ld_gather4(vrow(c));
       }
       part[t] = fmaf(q.x, kv.x, fmaf(q.y, kv.y, fmaf(q.z, kv.z, q.w * kv.w)));
     }
@@ -230,13 +244,13 @@ STC_DEVICE void attention_body(const AttnArgs& a) {
   }
 }
 
-template <int G, bool WRITE_S>
+template <int G, bool WRITE_S, bool NARROW>
 __global__ void __launch_bounds__(256) attention_kernel(AttnArgs a) {
-  attention_body<G, WRITE_S, false>(a);
+  attention_body<G, WRITE_S, false, NARROW>(a);
 }
-template <int G>
+template <int G, bool NARROW>
 __global__ void __launch_bounds__(256, STC_ATTN_VSMEM_MINB) attention_vsmem_kernel(AttnArgs a) {
-  attention_body<G, false, true>(a);
+  attention_body<G, false, true, NARROW>(a);
 }
 
 }  // namespace stc
