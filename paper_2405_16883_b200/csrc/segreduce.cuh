@@ -27,6 +27,10 @@
 
 #include "stc_common.cuh"
 
+#ifndef STC_SPMM_LANE_OFF
+#define STC_SPMM_LANE_OFF 2
+#endif
+
 namespace stc {
 
 #ifdef STC_DBG_TIMING
@@ -82,7 +86,24 @@ struct SpmmOp {
   STC_DEVICE Item shfl(const Item& it, int src, unsigned mask) const {
     return Item{__shfl_sync(mask, it.off, src, SUBW), __shfl_sync(mask, it.v, src, SUBW)};
   }
+#if STC_SPMM_LANE_OFF == 1
+  // keep the lane's column offset in a register: without this it is recomputed for every gather
+  // from %ctaid.y (an S2R and two integer ops on the address path of each entry)
+  STC_DEVICE void shift(int col0) {
+    lane_off = (unsigned)col0;
+    asm volatile("" : "+r"(lane_off));
+  }
+#elif STC_SPMM_LANE_OFF == 2
+  // ... or fold it into the operand base, held as an opaque 64-bit register
+  STC_DEVICE void shift(int col0) {
+    B += col0;
+    limit -= (unsigned)col0 <= limit ? (unsigned)col0 : limit;
+    asm volatile("" : "+l"(B));
+    lane_off = 0;
+  }
+#else
   STC_DEVICE void shift(int col0) { lane_off = (unsigned)col0; }
+#endif
   STC_DEVICE void fetch(const Item& it, Pre& pre) const {
     STC_CHECK((unsigned long long)(it.off + lane_off) + VEC <= limit, "SpMM gather outside B");
     pre.b.load_gather(B + (it.off + lane_off));
